@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""bench.py — 2DSW cell-updates/s on B200 (BASELINE.json metric) + roofline.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...    (one rank per GPU)
+
+Workload: BASELINE.json configs[4], C5 — the weak
+scaling run, 16384 x 16384 cells per GPU (global nx = 16384, ny = 16384 N),
+wet/dry bowl with islands, closed basin, dx = dy = 1 m, dt = 0.01 s, with the
+per-step global-volume reduction fused into the step.  It is the one config
+that spans 1/2/4/8 B200 and whose state (7.5 GB per GPU) is far larger than
+L2, as the "% of HBM roofline" half of the metric needs.  One bench step =
+one sw2d_step(T) call = T = 100 model time steps (the paper's time loop,
+PAPER.md:369-385); value = global cells * T * K / time.
+
+`value`: device-resident state, CUDA events on the handle's stream around K
+bench steps, barrier + synchronize on both sides, max over ranks.
+`e2e`: the same metric through the public C ABI with host buffers: every
+bench step uploads the state from pinned host memory (sw2d_set_state), runs
+T steps and reads the T per-step volumes back (sw2d_reduce_history).
+`--impl reference`: the CPU oracle (oracle/, single-threaded C) timed on a
+bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sw2d_inputs as si  # noqa: E402
+
+METRIC = "2DSW cell-updates/s at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "cell-updates/s"
+BYTES_PER_CELL = 28          # fused step: read eta,u,v,hzero (16 B) + write eta,u,v (12 B)
+FALLBACK_HBM_GBS = 6650.0    # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4"], default="c5")
+    ap.add_argument("--substeps", type=int, default=None,
+                    help="model time steps per bench step (default 100; c2: 10000)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="short run for ncu: no e2e / cpu baseline / clocks")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch of the step kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def default_substeps(workload):
+    return 10000 if workload == "c2" else 100
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle on a bounded sample of the same workload
+# ---------------------------------------------------------------------------
+
+def oracle_sample(cfg, target_s=4.0):
+    """A band of rows from the middle of the workload's grid (full width),
+    run as its own closed basin; sized for about target_s seconds per sample."""
+    import oracle
+    nx, ny = cfg["nx"], cfg["ny"]
+    rows = int(max(4, min(ny, 256)))
+    j0 = max(0, ny // 2 - rows // 2)
+    st = si.generate(cfg, j0=j0, nrows=rows)
+    params = si.model_params(cfg)
+    t = time.perf_counter()
+    oracle.run(params, *st, 1)
+    per_step = max(time.perf_counter() - t, 1e-6)
+    steps = int(max(1, min(1000, target_s / per_step)))
+    desc = (f"rows [{j0},{j0 + rows}) x all {nx} cols of {cfg['name']} run as a closed "
+            f"basin, {steps} steps per sample (single-threaded C oracle)")
+    return params, st, steps, rows * nx, desc
+
+
+def run_reference(args, cfg, ws, rank):
+    if rank != 0:
+        return
+    import oracle
+    params, st, steps, cells, desc = oracle_sample(cfg)
+    for _ in range(max(args.warmup, 0)):
+        oracle.run(params, *st, steps)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.run(params, *st, steps)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    value = cells * steps * args.steps / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(cfg, args, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": desc, "cpu": platform.processor() or platform.machine()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args, ws):
+    return {
+        "workload": f"{cfg['name']}: {cfg['desc']}",
+        "nx": cfg["nx"], "ny": cfg["ny"], "cells_per_gpu": cfg["nx"] * cfg["ny"] // ws,
+        "substeps_per_step": args.substeps, "dx": cfg["dx"], "dt": cfg["dt"],
+        "reduce_every_step": "VOLUME" if cfg["name"] in ("c5",) else "none",
+        "parallelism": f"row slabs x{ws}" if ws > 1 else "1 GPU",
+        "l2": "inputs larger than L2 (state >> 126 MB), no flush"
+        if cfg["nx"] * cfg["ny"] // ws * BYTES_PER_CELL > 1e9 else
+        "L2-resident working set (launch/latency-bound; no L2 flush)",
+    }
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, cfg, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_04471_b200 import sw2d
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny = cfg["nx"], cfg["ny"]
+    j0, nrows = sw2d.sw2d_partition(ny, ws, rank)
+    T = args.substeps
+    mask = (1 << sw2d.SW2D_RED_VOLUME) if cfg["name"] == "c5" else 0
+
+    # inputs for this rank's slab, in pinned host memory
+    host = [torch.empty((nrows, nx), dtype=torch.float32, pin_memory=True) for _ in range(4)]
+    si.generate(cfg, j0=j0, nrows=nrows, out=tuple(t.numpy() for t in host))
+
+    uid = None
+    if ws > 1:
+        obj = [sw2d.sw2d_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()          # the handle's stream; events are recorded on it
+    torch.cuda.set_stream(stream)
+    p = sw2d.make_params(nx, ny, cfg["dx"], cfg["dy"], cfg["dt"], cfg["g"], cfg["eps"],
+                         cfg["hmin"], reduce_every_step=mask, history_len=max(T, 1))
+    h = sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid), stream)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    try:
+        sw2d.sw2d_set_state(h, *host)
+        for _ in range(args.warmup):
+            sw2d.sw2d_step(h, T)
+        sw2d.sw2d_sync(h)
+
+        # --- value: state resident in HBM -------------------------------
+        l0 = sw2d.sw2d_launch_count(h)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with Clocks(local) as clk:
+            barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                sw2d.sw2d_step(h, T)
+            ev1.record(stream)
+            sw2d.sw2d_sync(h)
+            torch.cuda.synchronize()
+            barrier()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        launches = sw2d.sw2d_launch_count(h) - l0
+        value = nx * ny * T * args.steps / (ms * 1e-3)
+
+        # roofline of the step kernel (1 launch per model step at N=1; at N>1
+        # interior + boundary launches per step, timed together)
+        step_launches_per_model_step = launches / (T * args.steps)
+        t_step_s = ms * 1e-3 / (T * args.steps)
+        cells_local = nrows * nx
+        achieved = BYTES_PER_CELL * cells_local / t_step_s / 1e9
+        peak, peak_src = hbm_peak()
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
+                "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells_local,
+                "kernel": "sw2d_step_fused<1>" if mask else "sw2d_step_fused<0>",
+                "launches_per_model_step": step_launches_per_model_step,
+                "peak_source": peak_src,
+                "note": "per-model-step time of the whole timed region (the step kernel "
+                        "is the only kernel per step; its fused last-CTA fold included)"}
+
+        # --- e2e: host buffers through the C ABI ----------------------------
+        e2e = None
+        if not args.no_e2e and not args.profile:
+            hist = np.empty(T, np.float64)
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            for _ in range(args.steps):
+                sw2d.sw2d_set_state(h, *host)
+                sw2d.sw2d_step(h, T)
+                if mask:
+                    sw2d.sw2d_reduce_history(h, sw2d.SW2D_RED_VOLUME, T, hist)
+                else:
+                    sw2d.sw2d_reduce(h, sw2d.SW2D_RED_VOLUME)
+            e1.record(stream)
+            sw2d.sw2d_sync(h)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            barrier()
+            ems = max_over_ranks(e0.elapsed_time(e1))
+            e2e = {"value": nx * ny * T * args.steps / (ems * 1e-3), "unit": UNIT,
+                   "h2d_bytes_per_step": 16 * cells_local,
+                   "d2h_bytes_per_step": 8 * T if mask else 8,
+                   "ms_per_step": ems / args.steps, "wall_s": wall,
+                   "path": "sw2d_set_state(pinned host) + sw2d_step(T) + "
+                           "sw2d_reduce_history(VOLUME, T) per bench step"}
+    finally:
+        sw2d.sw2d_destroy(h)
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline and not args.profile:
+        import oracle
+        params, st, steps, cells, desc = oracle_sample(cfg)
+        t = time.perf_counter()
+        oracle.run(params, *st, steps)
+        dt_s = time.perf_counter() - t
+        cpu = {"value": cells * steps / dt_s, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": desc, "seconds": dt_s}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded bowl + islands + Gaussian bump)",
+        "config": workload_config(cfg, args, ws),
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "clocks": clk.summary(), "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.substeps is None:
+        args.substeps = default_substeps(args.workload)
+    cfg = si.config(args.workload, ws if args.workload == "c5" else 1)
+    if args.impl == "reference":
+        run_reference(args, cfg, ws, rank)
+        return
+    run_ours(args, cfg, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

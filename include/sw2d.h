@@ -1,0 +1,178 @@
+/* include/sw2d.h — C ABI of the B200-native 2-D shallow water (2DSW) time step.
+ *
+ * The operation: the time step of the 2DSW model that arXiv 1711.04471's
+ * compiler offloads as map kernels: "a time loop which calls two subroutines,
+ * a predictor (dyn) and a first-order Shapiro filter (shapiro), before
+ * updating the velocity ... transforms this code into three map-style kernels"
+ * (§6.2), run "for 10,000 time steps ... spatial resolution
+ * of 1 m and a time step of 0.01 s".  The scheme (the cited
+ * textbook's C-grid wet/dry scheme) and every reading of the paper are written
+ * out in DESIGN.md ("Oracle step", readings R1-R21).
+ *
+ * The calls are the domain-level form of the paper's host runtime contract
+ * (init, buffer-create, write-buffer, read-buffer, run-kernel,
+ * finish) with the paper's transfer minimisation (transfers
+ * "made only once in the run"): state is uploaded once by sw2d_set_state and
+ * sw2d_step(n) performs no host<->device transfer.
+ *
+ * Grid and layout (all calls):
+ *   nx x ny interior cells; x runs along columns k, y along rows j.
+ *   Arakawa C-grid: eta, hzero, wet at cell centres; u[j][k] on the face east
+ *   of cell (j,k) (k = nx-1 is the east wall), v[j][k] on the face north of
+ *   cell (j,k) (j = ny-1 is the north wall).  West/south walls are implicit
+ *   zero faces.  Boundary: closed basin (SW2D_BC_CLOSED).
+ *   Host-visible arrays are row-major float32 [nrows][nx] views of the rows
+ *   [j0, j0+nrows) this handle owns (the whole grid for one GPU or virtual
+ *   ranks): a[(j - j0) * nx + k], 0-based.  Wall-face entries of u and v are
+ *   ignored on input and are 0 on output.
+ *
+ * Ownership: the caller owns every buffer it passes and the library only
+ * reads/writes it during the call (it copies).  Pointers may be host
+ * (pageable or pinned) or device (CUDA UVA) memory.  The library owns its
+ * device memory, its NCCL communicator and, unless the caller passes one, its
+ * CUDA stream.  A handle is not thread-safe: one handle per (process, device).
+ *
+ * Errors: every int-returning call returns SW2D_OK (0) or a negative status;
+ * nothing aborts and no C++ exception crosses this boundary.  CUDA and NCCL
+ * failures are sticky (every later call returns the same status).
+ * sw2d_last_error() holds a one-line description of the last failure.
+ */
+#ifndef SW2D_H
+#define SW2D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW2D_ABI_VERSION 1
+
+typedef struct sw2d sw2d; /* opaque, library-owned */
+
+enum {
+  SW2D_OK = 0,
+  SW2D_EINVAL = -1,      /* bad parameter, non-finite input, nrows < 4 per rank */
+  SW2D_ENOMEM = -2,      /* device allocation failed                           */
+  SW2D_ECUDA = -3,       /* CUDA error (sticky)                                */
+  SW2D_ENCCL = -4,       /* NCCL error or NCCL unavailable (sticky)            */
+  SW2D_ESTATE = -5,      /* step/reduce/get before set_state                   */
+  SW2D_EUNSUPPORTED = -6 /* e.g. bc != SW2D_BC_CLOSED                          */
+};
+
+enum { SW2D_BC_CLOSED = 0 };
+
+/* Diagnostics (reading R16; none in the paper — SPEC.md:406 "0 fold
+ * kernels" — the north_star's "global sums and maxima"). */
+enum {
+  SW2D_RED_VOLUME = 0,    /* dx*dy*sum(hzero + eta) over interior cells, fp64     */
+  SW2D_RED_SUM_ETA = 1,   /* sum(eta), fp64                                        */
+  SW2D_RED_MAX_ETA = 2,   /* max eta (exact fp32 value)                            */
+  SW2D_RED_MIN_ETA = 3,   /* min eta                                               */
+  SW2D_RED_MAX_ABS_U = 4, /* max |u| over faces                                    */
+  SW2D_RED_MAX_ABS_V = 5, /* max |v|                                               */
+  SW2D_RED_WET_COUNT = 6, /* number of wet cells (wet = !(hzero+eta < hmin))       */
+  SW2D_RED_N = 7
+};
+
+/* Step-kernel variants (sw2d_params.variant). */
+enum {
+  SW2D_VARIANT_FUSED = 0 /* one fused pass per step: 28 B/cell-step */
+};
+
+typedef struct {
+  int64_t nx, ny;      /* global interior cells, >= 1 each                        */
+  float dx, dy, dt;    /* > 0, finite (m, m, s); paper: 1 m, 1 m, 0.01 s          */
+  float g;             /* >= 0, finite (g = 0: Shapiro filter only, used by tests) */
+  float eps;           /* Shapiro coefficient, 0 <= eps <= 1                      */
+  float hmin;          /* wet threshold (m) >= 0: wet iff !(hzero+eta < hmin)     */
+  int32_t bc;          /* SW2D_BC_CLOSED                                          */
+  uint32_t reduce_every_step; /* bitmask of (1u << SW2D_RED_*) computed inside
+                                 every step (fused epilogue) into a history ring */
+  int32_t variant;     /* SW2D_VARIANT_*                                          */
+  int32_t history_len; /* ring capacity in steps for per-step reductions; 0 ->
+                          default 1024                                            */
+} sw2d_params;
+
+typedef struct {
+  int32_t rank, nranks;  /* row slabs along y (balanced); nrows >= 4 per rank     */
+  int32_t device;        /* CUDA ordinal for this rank (-1: current device)       */
+  int32_t virtual_ranks; /* 1: run all nranks slabs in this one handle on one
+                            device, halos copied device-to-device (no NCCL); the
+                            handle then owns the whole grid (test mode)          */
+  unsigned char nccl_id[128]; /* ncclUniqueId from rank 0 (sw2d_nccl_unique_id),
+                                 broadcast by the caller (e.g. torch.distributed) */
+} sw2d_dist;
+
+/* Library ABI version (SW2D_ABI_VERSION of the built library). */
+int sw2d_abi_version(void);
+
+/* Pure host: rows [*j0, *j0 + *nrows) (0-based) of rank `rank` among `nranks`
+ * balanced row slabs of a grid with ny rows.  SW2D_EINVAL if nranks < 1, rank
+ * out of range, or a slab would have fewer than 4 rows (nranks > 1). */
+int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
+                   int64_t* nrows);
+
+/* Pure host: writes a fresh ncclUniqueId (128 bytes) for sw2d_dist.nccl_id.
+ * SW2D_ENCCL if NCCL cannot be loaded. */
+int sw2d_nccl_unique_id(unsigned char out[128]);
+
+/* Create a handle.  dist == NULL: one GPU (the current device), whole grid.
+ * cuda_stream: a cudaStream_t to enqueue on (e.g. torch's current stream), or
+ * NULL for a library-owned stream.  Allocates 7 device arrays (hzero and
+ * double-buffered eta, u, v) of (nrows + 4) x pitch floats.  *out = NULL on
+ * failure. */
+int sw2d_create(const sw2d_params* params, const sw2d_dist* dist,
+                void* cuda_stream, sw2d** out);
+
+/* Rows [*j0, *j0 + *nrows) (0-based, global) whose state this handle holds. */
+int sw2d_local_rows(const sw2d* h, int64_t* j0, int64_t* nrows);
+
+/* Upload the state (the paper's once-per-run write-buffer): hzero, eta, u, v
+ * as [nrows][nx] float32 (see layout above).  u and v may be NULL (= 0).
+ * Synchronous.  SW2D_EINVAL if any interior value is non-finite.  Resets the
+ * step counter and the reduction history.  With nranks > 1 every rank must
+ * call it (it exchanges the static hzero halo once). */
+int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
+                   const float* u, const float* v);
+
+/* Enqueue nsteps >= 0 time steps on the handle's stream; returns before they
+ * complete.  No host<->device transfer.  With nranks > 1 it exchanges the
+ * 2-row halos each step (NCCL send/recv) and, if reduce_every_step != 0,
+ * allreduces the per-step diagnostics. */
+int sw2d_step(sw2d* h, int64_t nsteps);
+
+/* The global value of diagnostic `op` (SW2D_RED_*) of the current state, on
+ * every rank.  Synchronizes. */
+int sw2d_reduce(sw2d* h, int op, double* out);
+
+/* The per-step values of diagnostic `op` for the last n steps (oldest first),
+ * n <= min(steps taken since set_state, history_len); op must be in
+ * reduce_every_step.  Synchronizes. */
+int sw2d_reduce_history(sw2d* h, int op, double* out, int64_t n);
+
+/* Download the state rows this handle holds: eta, u, v [nrows][nx] float32 and
+ * wet [nrows][nx] uint8 (0/1).  Any pointer may be NULL.  Synchronizes. */
+int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet);
+
+/* Wait for all enqueued work of this handle. */
+int sw2d_sync(sw2d* h);
+
+/* Number of this library's kernel launches enqueued since create (all kinds);
+ * -1 if h is NULL. */
+int64_t sw2d_launch_count(const sw2d* h);
+
+/* Destroy the handle and free its device memory / communicator.  NULL-safe. */
+void sw2d_destroy(sw2d* h);
+
+/* Static description of a status code. */
+const char* sw2d_strerror(int code);
+
+/* Detail of the last failing call on h (empty string if none; h may be NULL
+ * for the last sw2d_create failure in this thread). */
+const char* sw2d_last_error(const sw2d* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SW2D_H */

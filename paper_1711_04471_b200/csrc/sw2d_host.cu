@@ -1,0 +1,764 @@
+// paper_1711_04471_b200/csrc/sw2d_host.cu — host runtime behind include/sw2d.h.
+//
+// Owns the device state of one handle (one GPU, or all virtual ranks on one
+// GPU), plans the step-kernel launches, runs the time loop without host
+// transfers (the paper's once-per-run transfer rule), moves
+// the 2-row halos between row slabs (NCCL send/recv over NVLink between
+// ranks, device copies between virtual ranks) and folds the diagnostics.
+// See DESIGN.md "Host runtime" and "Multi-GPU".
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sw2d.h"
+#include "sw2d_internal.cuh"
+#include "sw2d_nccl.cuh"
+
+using namespace sw2d_dev;
+
+namespace {
+
+thread_local std::string t_create_err;
+
+constexpr int kMinRowsPerSeg = 8;
+constexpr int kDefaultHistory = 1024;
+
+struct Slab {
+  int64_t j0 = 0, nrows = 0;  // 0-based global first owned row, owned rows
+  float* H0 = nullptr;
+  float* E[2] = {nullptr, nullptr};
+  float* U[2] = {nullptr, nullptr};
+  float* V[2] = {nullptr, nullptr};
+};
+
+// One step-kernel launch over a band of rows of one slab.
+struct Launch {
+  int slab;
+  long long row_lo, row_hi;  // global 1-based rows, inclusive
+  int rows_per_seg, nsegs, blocks, part_base;
+  int phase;                 // 0: needs no halo of this step; 1: after the halo exchange
+};
+
+}  // namespace
+
+struct sw2d {
+  sw2d_params p{};
+  Coef coef{};
+  int rank = 0, nranks = 1;
+  bool virt = false, multi = false;  // multi: real ranks with NCCL
+  int device = 0;
+  int64_t pitch = 0;
+  int nstrips = 0;
+  int red_level = 0;
+  std::vector<Slab> slabs;
+  std::vector<Launch> launches;
+  int step_blocks = 0;
+  int cur = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  RedPartial* partials = nullptr;
+  int partials_cap = 0;
+  unsigned int* counter = nullptr;
+  double* hist = nullptr;
+  int hist_len = 0;
+  double* rec = nullptr;    // scratch record (ingest, sw2d_reduce)
+  double* h0sum = nullptr;  // sum of hzero over the cells this handle owns
+  double* zero = nullptr;   // a device 0.0
+  int* bad = nullptr;
+  unsigned char* wetbuf = nullptr;
+  size_t wetbuf_bytes = 0;
+  int64_t steps = 0;
+  bool state_set = false;
+  bool pending_allreduce = false;
+  int64_t pending_step = 0;
+  int sticky = 0;
+  std::string err;
+  ncclComm_t comm_nccl = nullptr;
+  int64_t nlaunch = 0;
+};
+
+namespace {
+
+int fail(sw2d* h, int code, const std::string& msg) {
+  if (h) {
+    h->err = msg;
+    if (code == SW2D_ECUDA || code == SW2D_ENCCL) h->sticky = code;
+  } else {
+    t_create_err = msg;
+  }
+  return code;
+}
+
+#define CUDA_TRY(h, call)                                                   \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      return fail((h), e_ == cudaErrorMemoryAllocation ? SW2D_ENOMEM        \
+                                                       : SW2D_ECUDA,        \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define NCCL_TRY(h, call)                                                   \
+  do {                                                                      \
+    ncclResult_t r_ = (call);                                               \
+    if (r_ != ncclSuccess)                                                  \
+      return fail((h), SW2D_ENCCL,                                          \
+                  std::string(#call) + ": " +                               \
+                      sw2d_host::nccl().GetErrorString(r_));                \
+  } while (0)
+
+#define ENTER(h)                                                  \
+  do {                                                            \
+    if (!(h)) return SW2D_EINVAL;                                 \
+    if ((h)->sticky) return (h)->sticky;                          \
+    CUDA_TRY((h), cudaSetDevice((h)->device));                    \
+  } while (0)
+
+bool finite_pos(float x) { return std::isfinite(x) && x > 0.0f; }
+
+int validate(const sw2d_params* p, std::string& why) {
+  if (!p) { why = "params is NULL"; return SW2D_EINVAL; }
+  if (p->bc != SW2D_BC_CLOSED) { why = "bc must be SW2D_BC_CLOSED"; return SW2D_EUNSUPPORTED; }
+  if (p->variant != SW2D_VARIANT_FUSED) { why = "unknown variant"; return SW2D_EUNSUPPORTED; }
+  if (p->nx < 1 || p->ny < 1) { why = "nx, ny must be >= 1"; return SW2D_EINVAL; }
+  if (p->nx > (1LL << 30)) { why = "nx too large"; return SW2D_EINVAL; }
+  if (!finite_pos(p->dx) || !finite_pos(p->dy) || !finite_pos(p->dt)) {
+    why = "dx, dy, dt must be finite and > 0"; return SW2D_EINVAL;
+  }
+  if (!std::isfinite(p->g) || p->g < 0.0f) { why = "g must be finite and >= 0"; return SW2D_EINVAL; }
+  if (!(p->eps >= 0.0f && p->eps <= 1.0f)) { why = "eps must be in [0, 1]"; return SW2D_EINVAL; }
+  if (!std::isfinite(p->hmin) || p->hmin < 0.0f) { why = "hmin must be finite and >= 0"; return SW2D_EINVAL; }
+  if (p->reduce_every_step >> SW2D_RED_N) { why = "unknown reduction bit"; return SW2D_EINVAL; }
+  if (p->history_len < 0) { why = "history_len must be >= 0"; return SW2D_EINVAL; }
+  return SW2D_OK;
+}
+
+// Coefficients once, in double, one rounding each (reading R12).
+Coef make_coef(const sw2d_params& p) {
+  Coef c;
+  const double t = (double)p.dt * (double)p.g;
+  c.cgx = (float)(-(t / (double)p.dx));
+  c.cgy = (float)(-(t / (double)p.dy));
+  c.cx = (float)((double)p.dt / (double)p.dx);
+  c.cy = (float)((double)p.dt / (double)p.dy);
+  c.q = 0.25f * p.eps;
+  c.hmin = p.hmin;
+  return c;
+}
+
+int red_level_of(uint32_t mask) {
+  const uint32_t sums = (1u << SW2D_RED_VOLUME) | (1u << SW2D_RED_SUM_ETA);
+  if (mask & ~sums) return 2;
+  if (mask & sums) return 1;
+  return 0;
+}
+
+float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch; }
+
+void plan_launches(sw2d* h) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  const int bps = step_occupancy_blocks_per_sm(h->red_level);
+  const long long resident_warps = (long long)sms * bps * kWarpsPerBlock;
+  const long long target_segs = std::max(1LL, resident_warps / h->nstrips);
+  h->launches.clear();
+  int part = 0;
+  auto add = [&](int s, long long lo, long long hi, int phase) {
+    if (hi < lo) return;
+    const long long rows = hi - lo + 1;
+    long long rps = (rows + target_segs - 1) / target_segs;
+    rps = std::max<long long>(rps, kMinRowsPerSeg);
+    Launch L;
+    L.slab = s;
+    L.row_lo = lo;
+    L.row_hi = hi;
+    L.rows_per_seg = (int)rps;
+    L.nsegs = (int)((rows + rps - 1) / rps);
+    L.phase = phase;
+    const long long warps = (long long)L.nsegs * h->nstrips;
+    L.blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    L.part_base = part;
+    part += L.blocks;
+    h->launches.push_back(L);
+  };
+  for (int s = 0; s < (int)h->slabs.size(); ++s) {
+    const Slab& sl = h->slabs[s];
+    const long long J0 = sl.j0 + 1, J1 = sl.j0 + sl.nrows;
+    if (h->multi) {
+      const bool lo_halo = h->rank > 0, hi_halo = h->rank < h->nranks - 1;
+      add(s, J0 + (lo_halo ? 2 : 0), J1 - (hi_halo ? 2 : 0), 0);
+      if (lo_halo) add(s, J0, J0 + 1, 1);
+      if (hi_halo) add(s, J1 - 1, J1, 1);
+    } else {
+      add(s, J0, J1, 0);
+    }
+  }
+  h->step_blocks = part;
+}
+
+StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
+  const Slab& sl = h->slabs[L.slab];
+  StepArgs a;
+  a.s.E = sl.E[h->cur];
+  a.s.U = sl.U[h->cur];
+  a.s.V = sl.V[h->cur];
+  a.s.H0 = sl.H0;
+  a.s.En = sl.E[1 - h->cur];
+  a.s.Un = sl.U[1 - h->cur];
+  a.s.Vn = sl.V[1 - h->cur];
+  a.s.pitch = h->pitch;
+  a.s.jbase = sl.j0 + 1 - kHaloRows;
+  a.nx = (int)h->p.nx;
+  a.ny = h->p.ny;
+  a.row_lo = L.row_lo;
+  a.row_hi = L.row_hi;
+  a.rows_per_seg = L.rows_per_seg;
+  a.nstrips = h->nstrips;
+  a.nsegs = L.nsegs;
+  a.c = h->coef;
+  a.red.partials = h->partials;
+  a.red.part_base = L.part_base;
+  a.red.counter = h->counter;
+  a.red.expected = h->step_blocks;
+  a.red.rec = rec;
+  a.red.h0sum = h->h0sum;
+  a.red.dxdy = (double)h->p.dx * (double)h->p.dy;
+  return a;
+}
+
+// Device copies of the 2-row halos between virtual-rank slabs (fields of
+// buffer `b`; hzero when b < 0).
+int virtual_halo(sw2d* h, int b) {
+  const size_t bytes = (size_t)(2 * h->pitch) * sizeof(float);
+  for (size_t s = 0; s + 1 < h->slabs.size(); ++s) {
+    Slab& lo = h->slabs[s];
+    Slab& hi = h->slabs[s + 1];
+    float* fl[3];
+    float* fh[3];
+    int nf = 3;
+    if (b < 0) {
+      fl[0] = lo.H0; fh[0] = hi.H0; nf = 1;
+    } else {
+      fl[0] = lo.E[b]; fl[1] = lo.U[b]; fl[2] = lo.V[b];
+      fh[0] = hi.E[b]; fh[1] = hi.U[b]; fh[2] = hi.V[b];
+    }
+    for (int f = 0; f < nf; ++f) {
+      CUDA_TRY(h, cudaMemcpyAsync(fld(fh[f], h->pitch, 0), fld(fl[f], h->pitch, lo.nrows),
+                                  bytes, cudaMemcpyDeviceToDevice, h->stream));
+      CUDA_TRY(h, cudaMemcpyAsync(fld(fl[f], h->pitch, lo.nrows + 2), fld(fh[f], h->pitch, 2),
+                                  bytes, cudaMemcpyDeviceToDevice, h->stream));
+    }
+  }
+  return SW2D_OK;
+}
+
+// NCCL exchange of the 2-row halos with the row neighbours (fields of buffer
+// `b`; hzero when b < 0), enqueued on stream `st`.
+int nccl_halo(sw2d* h, int b, cudaStream_t st) {
+  const auto& nc = sw2d_host::nccl();
+  Slab& sl = h->slabs[0];
+  float* f[3];
+  int nf = 3;
+  if (b < 0) {
+    f[0] = sl.H0; nf = 1;
+  } else {
+    f[0] = sl.E[b]; f[1] = sl.U[b]; f[2] = sl.V[b];
+  }
+  const size_t cnt = (size_t)(2 * h->pitch);
+  NCCL_TRY(h, nc.GroupStart());
+  for (int i = 0; i < nf; ++i) {
+    if (h->rank > 0) {  // south neighbour
+      NCCL_TRY(h, nc.Send(fld(f[i], h->pitch, 2), cnt, ncclFloat32, h->rank - 1, h->comm_nccl, st));
+      NCCL_TRY(h, nc.Recv(fld(f[i], h->pitch, 0), cnt, ncclFloat32, h->rank - 1, h->comm_nccl, st));
+    }
+    if (h->rank < h->nranks - 1) {  // north neighbour
+      NCCL_TRY(h, nc.Send(fld(f[i], h->pitch, sl.nrows), cnt, ncclFloat32, h->rank + 1, h->comm_nccl, st));
+      NCCL_TRY(h, nc.Recv(fld(f[i], h->pitch, sl.nrows + 2), cnt, ncclFloat32, h->rank + 1, h->comm_nccl, st));
+    }
+  }
+  NCCL_TRY(h, nc.GroupEnd());
+  return SW2D_OK;
+}
+
+// In-place allreduce of a 7-double record: sums [0..2], maxima [3..6].
+int nccl_allreduce_rec(sw2d* h, double* rec, cudaStream_t st) {
+  const auto& nc = sw2d_host::nccl();
+  NCCL_TRY(h, nc.GroupStart());
+  NCCL_TRY(h, nc.AllReduce(rec, rec, 3, ncclFloat64, ncclSum, h->comm_nccl, st));
+  NCCL_TRY(h, nc.AllReduce(rec + 3, rec + 3, 4, ncclFloat64, ncclMax, h->comm_nccl, st));
+  NCCL_TRY(h, nc.GroupEnd());
+  return SW2D_OK;
+}
+
+double rec_value(const double* rec, int op) {
+  switch (op) {
+    case SW2D_RED_VOLUME: return rec[kRecVol];
+    case SW2D_RED_SUM_ETA: return rec[kRecSumEta];
+    case SW2D_RED_MAX_ETA: return rec[kRecMaxEta];
+    case SW2D_RED_MIN_ETA: return -rec[kRecNegMinEta];
+    case SW2D_RED_MAX_ABS_U: return rec[kRecMaxU];
+    case SW2D_RED_MAX_ABS_V: return rec[kRecMaxV];
+    default: return rec[kRecWet];
+  }
+}
+
+void free_all(sw2d* h) {
+  for (Slab& s : h->slabs) {
+    cudaFree(s.H0);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(s.E[b]);
+      cudaFree(s.U[b]);
+      cudaFree(s.V[b]);
+    }
+  }
+  h->slabs.clear();
+  cudaFree(h->partials);
+  cudaFree(h->counter);
+  cudaFree(h->hist);
+  cudaFree(h->rec);
+  cudaFree(h->h0sum);
+  cudaFree(h->zero);
+  cudaFree(h->bad);
+  cudaFree(h->wetbuf);
+  if (h->ev_ready) cudaEventDestroy(h->ev_ready);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+  if (h->comm) cudaStreamDestroy(h->comm);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  if (h->comm_nccl && sw2d_host::nccl().ok) sw2d_host::nccl().CommDestroy(h->comm_nccl);
+}
+
+int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
+                void* cuda_stream) {
+  h->p = *params;
+  if (h->p.history_len == 0) h->p.history_len = kDefaultHistory;
+  h->coef = make_coef(h->p);
+  h->red_level = red_level_of(h->p.reduce_every_step);
+  h->hist_len = h->p.history_len;
+  if (dist) {
+    if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)
+      return fail(h, SW2D_EINVAL, "bad rank / nranks");
+    h->rank = dist->rank;
+    h->nranks = dist->nranks;
+    h->virt = dist->virtual_ranks != 0;
+    h->multi = !h->virt && h->nranks > 1;
+    if (dist->device >= 0) CUDA_TRY(h, cudaSetDevice(dist->device));
+  }
+  CUDA_TRY(h, cudaGetDevice(&h->device));
+  // slabs
+  if (h->virt) {
+    for (int r = 0; r < h->nranks; ++r) {
+      Slab s;
+      if (sw2d_partition(h->p.ny, h->nranks, r, &s.j0, &s.nrows) != SW2D_OK)
+        return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 4 rows per rank)");
+      h->slabs.push_back(s);
+    }
+  } else {
+    Slab s;
+    if (sw2d_partition(h->p.ny, h->nranks, h->rank, &s.j0, &s.nrows) != SW2D_OK)
+      return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 4 rows per rank)");
+    h->slabs.push_back(s);
+  }
+  h->nstrips = (int)((h->p.nx + kColsPerStrip - 1) / kColsPerStrip);
+  const int64_t need = (int64_t)h->nstrips * kColsPerStrip + 8;
+  h->pitch = (need + 31) / 32 * 32;
+  // streams
+  if (cuda_stream) {
+    h->stream = (cudaStream_t)cuda_stream;
+  } else {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
+  CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
+  if (h->multi) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
+  // fields: (nrows + 4) x pitch floats each, zeroed (halo rows / columns stay 0)
+  for (Slab& s : h->slabs) {
+    const size_t bytes = (size_t)(s.nrows + 2 * kHaloRows) * (size_t)h->pitch * sizeof(float);
+    float** all[7] = {&s.H0, &s.E[0], &s.E[1], &s.U[0], &s.U[1], &s.V[0], &s.V[1]};
+    for (float** f : all) {
+      CUDA_TRY(h, cudaMalloc(f, bytes));
+      CUDA_TRY(h, cudaMemsetAsync(*f, 0, bytes, h->stream));
+    }
+  }
+  plan_launches(h);
+  // reduction scratch
+  long long cap = h->step_blocks;
+  for (const Slab& s : h->slabs) {
+    IngestArgs ia{};
+    ia.nrows = s.nrows;
+    ia.nx = (int)h->p.nx;
+    ReduceArgs ra{};
+    ra.nrows = s.nrows;
+    ra.nx = (int)h->p.nx;
+    cap = std::max<long long>(cap, (long long)ingest_blocks(ia) * (long long)h->slabs.size());
+    cap = std::max<long long>(cap, (long long)reduce_blocks(ra) * (long long)h->slabs.size());
+  }
+  h->partials_cap = (int)cap;
+  CUDA_TRY(h, cudaMalloc(&h->partials, sizeof(RedPartial) * (size_t)cap));
+  CUDA_TRY(h, cudaMalloc(&h->counter, sizeof(unsigned int)));
+  CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->stream));
+  CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
+  CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
+  CUDA_TRY(h, cudaMalloc(&h->rec, sizeof(double) * kRecN));
+  CUDA_TRY(h, cudaMalloc(&h->h0sum, sizeof(double)));
+  CUDA_TRY(h, cudaMalloc(&h->zero, sizeof(double)));
+  CUDA_TRY(h, cudaMemsetAsync(h->zero, 0, sizeof(double), h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->h0sum, 0, sizeof(double), h->stream));
+  CUDA_TRY(h, cudaMalloc(&h->bad, sizeof(int)));
+  // NCCL communicator
+  if (h->multi) {
+    const auto& nc = sw2d_host::nccl();
+    if (!nc.ok) return fail(h, SW2D_ENCCL, std::string("NCCL unavailable: ") + nc.why);
+    ncclUniqueId id;
+    std::memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
+    NCCL_TRY(h, nc.CommInitRank(&h->comm_nccl, h->nranks, id, h->rank));
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return SW2D_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sw2d_abi_version(void) { return SW2D_ABI_VERSION; }
+
+int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
+                   int64_t* nrows) {
+  if (!j0 || !nrows || nranks < 1 || rank < 0 || rank >= nranks || ny < 1)
+    return SW2D_EINVAL;
+  const int64_t base = ny / nranks, rem = ny % nranks;
+  const int64_t n = base + (rank < rem ? 1 : 0);
+  if (nranks > 1 && base < 4) return SW2D_EINVAL;  // the smallest slab
+  *j0 = (int64_t)rank * base + std::min<int64_t>(rank, rem);
+  *nrows = n;
+  return SW2D_OK;
+}
+
+int sw2d_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return SW2D_EINVAL;
+  const auto& nc = sw2d_host::nccl();
+  if (!nc.ok) {
+    t_create_err = std::string("NCCL unavailable: ") + nc.why;
+    return SW2D_ENCCL;
+  }
+  ncclUniqueId id;
+  if (nc.GetUniqueId(&id) != ncclSuccess) {
+    t_create_err = "ncclGetUniqueId failed";
+    return SW2D_ENCCL;
+  }
+  std::memcpy(out, id.internal, sizeof(id.internal));
+  return SW2D_OK;
+}
+
+int sw2d_create(const sw2d_params* params, const sw2d_dist* dist,
+                void* cuda_stream, sw2d** out) {
+  if (!out) return SW2D_EINVAL;
+  *out = nullptr;
+  std::string why;
+  const int v = validate(params, why);
+  if (v != SW2D_OK) return fail(nullptr, v, why);
+  sw2d* h = new (std::nothrow) sw2d();
+  if (!h) return fail(nullptr, SW2D_ENOMEM, "host allocation failed");
+  const int rc = create_impl(h, params, dist, cuda_stream);
+  if (rc != SW2D_OK) {
+    t_create_err = h->err;
+    free_all(h);
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return SW2D_OK;
+}
+
+int sw2d_local_rows(const sw2d* h, int64_t* j0, int64_t* nrows) {
+  if (!h || !j0 || !nrows) return SW2D_EINVAL;
+  *j0 = h->slabs.front().j0;
+  *nrows = h->slabs.back().j0 + h->slabs.back().nrows - h->slabs.front().j0;
+  return SW2D_OK;
+}
+
+int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
+                   const float* u, const float* v) {
+  ENTER(h);
+  if (!hzero || !eta) return fail(h, SW2D_EINVAL, "hzero and eta are required");
+  const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
+  const size_t wbytes = (size_t)nx * sizeof(float);
+  const size_t dp = (size_t)h->pitch * sizeof(float);
+  CUDA_TRY(h, cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
+  for (Slab& s : h->slabs) {
+    const size_t src_off = (size_t)(s.j0 - hj0) * (size_t)nx;
+    float* dst[4] = {s.H0, s.E[0], s.U[0], s.V[0]};
+    const float* src[4] = {hzero, eta, u, v};
+    for (int f = 0; f < 4; ++f) {
+      float* d = dst[f] + kHaloRows * h->pitch + 1 + kColOff;
+      if (src[f]) {
+        CUDA_TRY(h, cudaMemcpy2DAsync(d, dp, src[f] + src_off, wbytes, wbytes,
+                                      (size_t)s.nrows, cudaMemcpyDefault, h->stream));
+      } else {
+        CUDA_TRY(h, cudaMemset2DAsync(d, dp, 0, wbytes, (size_t)s.nrows, h->stream));
+      }
+    }
+  }
+  // finiteness, wall faces, sum(hzero) — one fold over all slabs
+  int expected = 0;
+  std::vector<IngestArgs> ias;
+  for (Slab& s : h->slabs) {
+    IngestArgs a{};
+    a.E = s.E[0];
+    a.U = s.U[0];
+    a.V = s.V[0];
+    a.H0 = s.H0;
+    a.pitch = h->pitch;
+    a.jbase = s.j0 + 1 - kHaloRows;
+    a.nrows = s.nrows;
+    a.nx = (int)nx;
+    a.ny = h->p.ny;
+    a.bad = h->bad;
+    a.red.part_base = expected;
+    expected += ingest_blocks(a);
+    ias.push_back(a);
+  }
+  for (IngestArgs& a : ias) {
+    a.red.partials = h->partials;
+    a.red.counter = h->counter;
+    a.red.expected = expected;
+    a.red.rec = h->rec;
+    a.red.h0sum = h->zero;
+    a.red.dxdy = 0.0;
+    launch_ingest(a, h->stream);
+    h->nlaunch++;
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  CUDA_TRY(h, cudaMemcpyAsync(h->h0sum, h->rec + kRecSumEta, sizeof(double),
+                              cudaMemcpyDeviceToDevice, h->stream));
+  // static hzero halo, once
+  if (h->virt) {
+    int rc = virtual_halo(h, -1);
+    if (rc) return rc;
+  } else if (h->multi) {
+    int rc = nccl_halo(h, -1, h->stream);
+    if (rc) return rc;
+  }
+  int bad = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  h->cur = 0;
+  h->steps = 0;
+  h->pending_allreduce = false;
+  h->state_set = false;
+  if (bad) return fail(h, SW2D_EINVAL, "non-finite value in the input state");
+  CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
+  h->state_set = true;
+  return SW2D_OK;
+}
+
+int sw2d_step(sw2d* h, int64_t nsteps) {
+  ENTER(h);
+  if (nsteps < 0) return fail(h, SW2D_EINVAL, "nsteps must be >= 0");
+  if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_step before sw2d_set_state");
+  for (int64_t i = 0; i < nsteps; ++i) {
+    double* rec = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
+    if (h->virt) {
+      int rc = virtual_halo(h, h->cur);
+      if (rc) return rc;
+    }
+    if (h->multi) {
+      CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+      int rc = nccl_halo(h, h->cur, h->comm);
+      if (rc) return rc;
+      CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+      if (h->pending_allreduce) {  // previous step's diagnostics
+        rc = nccl_allreduce_rec(h, h->hist + (size_t)(h->pending_step % h->hist_len) * kRecN,
+                                h->comm);
+        if (rc) return rc;
+        h->pending_allreduce = false;
+      }
+    }
+    for (int phase = 0; phase < 2; ++phase) {
+      bool waited = false;
+      for (const Launch& L : h->launches) {
+        if (L.phase != phase) continue;
+        if (phase == 1 && !waited) {
+          CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+          waited = true;
+        }
+        launch_step(step_args(h, L, rec), h->red_level, h->stream);
+        h->nlaunch++;
+      }
+    }
+    CUDA_TRY(h, cudaGetLastError());
+    if (h->multi) {
+      CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
+      if (h->red_level) {
+        h->pending_allreduce = true;
+        h->pending_step = h->steps;
+      }
+    }
+    h->cur = 1 - h->cur;
+    h->steps++;
+  }
+  if (h->multi && h->pending_allreduce) {
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+    int rc = nccl_allreduce_rec(h, h->hist + (size_t)(h->pending_step % h->hist_len) * kRecN,
+                                h->comm);
+    if (rc) return rc;
+    h->pending_allreduce = false;
+    // later work on the compute stream (reads of the history) follows the allreduce
+    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+  }
+  return SW2D_OK;
+}
+
+int sw2d_sync(sw2d* h) {
+  ENTER(h);
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (h->comm) CUDA_TRY(h, cudaStreamSynchronize(h->comm));
+  if (h->multi) {
+    ncclResult_t ar = ncclSuccess;
+    NCCL_TRY(h, sw2d_host::nccl().CommGetAsyncError(h->comm_nccl, &ar));
+    NCCL_TRY(h, ar);
+  }
+  return SW2D_OK;
+}
+
+int sw2d_reduce(sw2d* h, int op, double* out) {
+  ENTER(h);
+  if (!out || op < 0 || op >= SW2D_RED_N) return fail(h, SW2D_EINVAL, "bad op / out");
+  if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_reduce before sw2d_set_state");
+  int expected = 0;
+  std::vector<ReduceArgs> ras;
+  for (Slab& s : h->slabs) {
+    ReduceArgs a{};
+    a.E = s.E[h->cur];
+    a.U = s.U[h->cur];
+    a.V = s.V[h->cur];
+    a.H0 = s.H0;
+    a.pitch = h->pitch;
+    a.nrows = s.nrows;
+    a.nx = (int)h->p.nx;
+    a.hmin = h->p.hmin;
+    a.red.part_base = expected;
+    expected += reduce_blocks(a);
+    ras.push_back(a);
+  }
+  for (ReduceArgs& a : ras) {
+    a.red.partials = h->partials;
+    a.red.counter = h->counter;
+    a.red.expected = expected;
+    a.red.rec = h->rec;
+    a.red.h0sum = h->h0sum;
+    a.red.dxdy = (double)h->p.dx * (double)h->p.dy;
+    launch_reduce(a, h->stream);
+    h->nlaunch++;
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  if (h->multi) {
+    int rc = nccl_allreduce_rec(h, h->rec, h->stream);
+    if (rc) return rc;
+  }
+  double rec[kRecN];
+  CUDA_TRY(h, cudaMemcpyAsync(rec, h->rec, sizeof(rec), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  *out = rec_value(rec, op);
+  return SW2D_OK;
+}
+
+int sw2d_reduce_history(sw2d* h, int op, double* out, int64_t n) {
+  ENTER(h);
+  if (!out || op < 0 || op >= SW2D_RED_N || n < 0)
+    return fail(h, SW2D_EINVAL, "bad op / out / n");
+  if (!(h->p.reduce_every_step & (1u << op)))
+    return fail(h, SW2D_EINVAL, "op not in reduce_every_step");
+  if (n > h->steps || n > h->hist_len)
+    return fail(h, SW2D_EINVAL, "n exceeds the steps taken or history_len");
+  if (n == 0) return SW2D_OK;
+  std::vector<double> ring((size_t)h->hist_len * kRecN);
+  CUDA_TRY(h, cudaMemcpyAsync(ring.data(), h->hist, ring.size() * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t step = h->steps - n + i;
+    out[i] = rec_value(ring.data() + (size_t)(step % h->hist_len) * kRecN, op);
+  }
+  return SW2D_OK;
+}
+
+int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
+  ENTER(h);
+  if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_get_state before sw2d_set_state");
+  const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
+  const size_t wbytes = (size_t)nx * sizeof(float);
+  const size_t dp = (size_t)h->pitch * sizeof(float);
+  int64_t total_rows = 0;
+  for (Slab& s : h->slabs) total_rows += s.nrows;
+  if (wet) {
+    const size_t need = (size_t)total_rows * (size_t)nx;
+    if (need > h->wetbuf_bytes) {
+      cudaFree(h->wetbuf);
+      h->wetbuf = nullptr;
+      h->wetbuf_bytes = 0;
+      CUDA_TRY(h, cudaMalloc(&h->wetbuf, need));
+      h->wetbuf_bytes = need;
+    }
+  }
+  for (Slab& s : h->slabs) {
+    const size_t off = (size_t)(s.j0 - hj0) * (size_t)nx;
+    float* dst[3] = {eta, u, v};
+    const float* src[3] = {s.E[h->cur], s.U[h->cur], s.V[h->cur]};
+    for (int f = 0; f < 3; ++f) {
+      if (!dst[f]) continue;
+      CUDA_TRY(h, cudaMemcpy2DAsync(dst[f] + off, wbytes,
+                                    src[f] + kHaloRows * h->pitch + 1 + kColOff, dp,
+                                    wbytes, (size_t)s.nrows, cudaMemcpyDefault, h->stream));
+    }
+    if (wet) {
+      launch_wet(s.E[h->cur], s.H0, h->pitch, s.nrows, (int)nx, h->p.hmin,
+                 h->wetbuf + off, h->stream);
+      h->nlaunch++;
+    }
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  if (wet)
+    CUDA_TRY(h, cudaMemcpyAsync(wet, h->wetbuf, (size_t)total_rows * (size_t)nx,
+                                cudaMemcpyDefault, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  return SW2D_OK;
+}
+
+int64_t sw2d_launch_count(const sw2d* h) { return h ? h->nlaunch : -1; }
+
+void sw2d_destroy(sw2d* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm) cudaStreamSynchronize(h->comm);
+  free_all(h);
+  delete h;
+}
+
+const char* sw2d_strerror(int code) {
+  switch (code) {
+    case SW2D_OK: return "ok";
+    case SW2D_EINVAL: return "invalid argument";
+    case SW2D_ENOMEM: return "out of device memory";
+    case SW2D_ECUDA: return "CUDA error";
+    case SW2D_ENCCL: return "NCCL error";
+    case SW2D_ESTATE: return "state not set";
+    case SW2D_EUNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+const char* sw2d_last_error(const sw2d* h) {
+  return h ? h->err.c_str() : t_create_err.c_str();
+}
+
+}  // extern "C"

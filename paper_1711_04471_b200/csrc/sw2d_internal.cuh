@@ -1,0 +1,120 @@
+// paper_1711_04471_b200/csrc/sw2d_internal.cuh — internal types shared by the
+// CUDA kernels (sw2d_kernels.cu) and the host runtime (sw2d_host.cu).
+//
+// Device layout: every field of a slab is a
+// row-major float32 array of (nrows + 4) rows x `pitch` floats.  Storage row
+// r holds global 1-based row j = jbase + r (jbase = first owned row - 2, so
+// two halo rows sit on each side).  Storage column c holds 1-based interior
+// column k = c - kColOff (k = 1 at c = 4: 16-byte aligned; the west wall
+// halo column k = 0 is c = 3).  pitch is a multiple of 32 floats (128 B).
+#pragma once
+#include <cstdint>
+
+namespace sw2d_dev {
+
+constexpr int kColOff = 3;           // storage column of 1-based column k is k + 3
+constexpr int kHaloRows = 2;         // halo rows per side (the fused step's cone)
+constexpr int kWarpsPerBlock = 4;
+constexpr int kThreads = 32 * kWarpsPerBlock;
+constexpr int kOutLanes = 30;        // lanes 1..30 produce output; 0 and 31 are halo lanes
+constexpr int kColsPerStrip = 4 * kOutLanes;   // 120 output columns per warp strip
+
+// Model coefficients, computed once on the host in double and rounded once
+// (reading R12).
+struct Coef {
+  float cgx, cgy, cx, cy, q, hmin;
+};
+
+// One slab's fields: state n (read) and state n+1 (written).
+struct SlabView {
+  const float* E;
+  const float* U;
+  const float* V;
+  const float* H0;
+  float* En;
+  float* Un;
+  float* Vn;
+  long long pitch;   // floats per storage row
+  long long jbase;   // global 1-based row of storage row 0
+};
+
+// Per-step diagnostics record (7 doubles, see SW2D_RED_*): the sum part
+// [0..2] and the max part [3..6] are allreduced separately across ranks.
+enum { kRecVol = 0, kRecSumEta = 1, kRecWet = 2, kRecMaxEta = 3,
+       kRecNegMinEta = 4, kRecMaxU = 5, kRecMaxV = 6, kRecN = 7 };
+
+// Per-CTA partial of the diagnostics.
+struct RedPartial {
+  double sum_eta;
+  double wet;
+  float max_eta, neg_min_eta, max_u, max_v;
+};
+
+struct RedArgs {
+  RedPartial* partials;      // one slot per CTA of the step (all launches)
+  int part_base;             // first slot of this launch
+  unsigned int* counter;     // CTAs done this step (reset by the last CTA)
+  int expected;              // CTAs writing partials this step (all launches)
+  double* rec;               // the step's 7-double record (written by last CTA)
+  const double* h0sum;       // sum of hzero over the cells this handle owns
+  double dxdy;
+};
+
+struct StepArgs {
+  SlabView s;
+  int nx;
+  long long ny;
+  long long row_lo, row_hi;  // global 1-based output rows of this launch (inclusive)
+  int rows_per_seg;          // output rows per warp segment
+  int nstrips;               // warp strips across the columns
+  int nsegs;                 // warp segments down the rows
+  Coef c;
+  RedArgs red;
+};
+
+// Kernel launchers (sw2d_kernels.cu).  `red_level`: 0 none, 1 sums
+// (VOLUME, SUM_ETA), 2 all diagnostics.
+int step_blocks(const StepArgs& a);
+void launch_step(const StepArgs& a, int red_level, void* stream);
+int step_occupancy_blocks_per_sm(int red_level);
+
+// set_state helper: checks finiteness of the interior, zeroes the wall faces
+// of U (k = nx) and V (global j = ny), and sums hzero in fp64 into *h0sum.
+struct IngestArgs {
+  float* E;
+  float* U;
+  float* V;
+  const float* H0;
+  long long pitch;
+  long long jbase;           // global 1-based row of storage row 0
+  long long nrows;           // owned rows (storage rows 2 .. nrows+1)
+  int nx;
+  long long ny;
+  int* bad;                  // set to 1 if any value is non-finite
+  RedArgs red;               // partials/counter/expected; result into *red.rec (1 double)
+};
+int ingest_blocks(const IngestArgs& a);
+void launch_ingest(const IngestArgs& a, void* stream);
+
+// Diagnostics of the current state (sw2d_reduce): same record as the fused
+// epilogue.  One launch per slab; all slabs of a handle share the counter.
+struct ReduceArgs {
+  const float* E;
+  const float* U;
+  const float* V;
+  const float* H0;
+  long long pitch;
+  long long nrows;
+  int nx;
+  float hmin;
+  RedArgs red;
+};
+int reduce_blocks(const ReduceArgs& a);
+void launch_reduce(const ReduceArgs& a, void* stream);
+
+// wet mask of the current state into a dense uint8 [nrows][nx] buffer.
+void launch_wet(const float* E, const float* H0, long long pitch,
+                long long nrows, int nx, float hmin, unsigned char* out,
+                void* stream);
+
+}  // namespace sw2d_dev

@@ -1,0 +1,295 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Element by element on the same seeded inputs (sw2d_inputs), at sizes the
+oracle finishes in seconds that span several warp strips (120 columns),
+several row segments and ragged tails; the full BASELINE sizes (C3 8192^2,
+C5 16384^2 in bench.py's launch configuration) on sampled windows the oracle
+computes exactly from the initial state, plus properties that hold at any
+size.  The bar (north_star): fields within 1e-5 of max |field| after 100
+steps — we require bitwise (same operation order, no FMA) —
+reductions 1e-5 relative (max/min/count exact), wet masks bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import sw2d_inputs as si
+from paper_1711_04471_b200 import sw2d
+from _parity import assert_state_equal, check_reductions, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+P = dict(si.PARAMS)
+ALL = (1 << sw2d.SW2D_RED_N) - 1
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    sw2d.load()
+
+
+def _bowl(nx, ny, seed=3, sigma=None):
+    cfg = dict(si.config("c3"), nx=nx, ny=ny, seed=seed,
+               sigma=sigma if sigma else max(2.0, min(nx, ny) / 16))
+    return cfg, si.generate(cfg)
+
+
+# --- full-field parity at oracle-sized grids ------------------------------
+
+@pytest.mark.parametrize("nsteps", [1, 100, 1000])
+def test_c1_bitwise(nsteps):
+    cfg = si.config("c1")
+    st = si.generate(cfg)
+    want = oracle_run(P, st, nsteps)
+    got, _, red, _ = gpu_run(P, st, nsteps)
+    assert_state_equal(got, want, where=f"C1 after {nsteps} steps")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+
+
+@pytest.mark.parametrize("nx,ny", [(517, 389), (241, 600), (120, 121), (1000, 37)])
+def test_wetdry_bowl_bitwise_ragged(nx, ny):
+    """Several 120-column strips with a ragged last strip, several row
+    segments with a ragged last one, shorelines and islands."""
+    cfg, st = _bowl(nx, ny)
+    want = oracle_run(P, st, 100)
+    got, _, red, _ = gpu_run(P, st, 100)
+    assert_state_equal(got, want, where=f"bowl {nx}x{ny}, 100 steps")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+
+
+def test_c2_paper_shape_bitwise():
+    cfg = si.config("c2")
+    st = si.generate(cfg)
+    want = oracle_run(P, st, 100)
+    got, _, _, _ = gpu_run(P, st, 100)
+    assert_state_equal(got, want, where="C2 500x500, 100 steps")
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (1, 9), (9, 1), (2, 3), (3, 3), (4, 4),
+                                   (5, 130), (119, 2), (121, 8), (240, 17)])
+def test_degenerate_and_tiny_grids(nx, ny):
+    rng = np.random.default_rng(nx * 1000 + ny)
+    hz = rng.uniform(-1.0, 3.0, (ny, nx)).astype(np.float32)
+    e = np.where(hz < 0, -hz, rng.uniform(-0.2, 0.4, (ny, nx))).astype(np.float32)
+    u = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
+    v = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
+    st = (hz, e, u, v)
+    want = oracle_run(P, st, 25)
+    got, _, red, _ = gpu_run(P, st, 25)
+    assert_state_equal(got, want, where=f"random {nx}x{ny}")
+    check_reductions(red, oracle.reduce(P, hz, *want[:3]))
+
+
+def test_golden_examples_through_the_abi():
+    """The hand-computed 3x3 example (tests/golden) on the GPU."""
+    hz = np.full((3, 3), 10.0, np.float32)
+    e = np.zeros((3, 3), np.float32)
+    e[1, 1] = 1.0
+    z = np.zeros_like(hz)
+    got, _, _, _ = gpu_run(P, (hz, e, z, z), 1)
+    assert abs(float(got[0][1, 1]) - 0.90953375) < 1e-6
+    assert abs(float(got[0][0, 1]) - 0.0223467875) < 1e-7
+    assert abs(float(got[1][1, 1]) - 0.0981) < 1e-7
+
+
+def test_lake_at_rest_bitwise_gpu():
+    rng = np.random.default_rng(5)
+    hz = rng.uniform(-2.0, 10.0, (300, 257)).astype(np.float32)
+    hz[rng.random(hz.shape) < 0.1] = np.float32(0.02)
+    hz[5, 7] = np.float32(P["hmin"])
+    e = (-np.minimum(np.float32(0.0), hz)).astype(np.float32)
+    z = np.zeros_like(hz)
+    got, _, _, _ = gpu_run(P, (hz, e, z, z), 500)
+    np.testing.assert_array_equal(got[0], e)
+    assert np.all(got[1] == 0) and np.all(got[2] == 0)
+
+
+# --- chunking, determinism, reductions ------------------------------------
+
+def test_step_chunking_is_invisible():
+    cfg, st = _bowl(300, 250)
+    a, _, _, _ = gpu_run(P, st, 60)
+    b, _, _, _ = gpu_run(P, st, 60, chunks=[1, 7, 0, 22, 30])
+    assert_state_equal(a, b, where="chunked vs one call")
+
+
+def test_determinism_run_to_run():
+    cfg, st = _bowl(700, 333)
+    a, ha, ra, _ = gpu_run(P, st, 50, reduce_mask=ALL)
+    b, hb, rb, _ = gpu_run(P, st, 50, reduce_mask=ALL)
+    assert_state_equal(a, b, where="run twice")
+    for op in ha:
+        np.testing.assert_array_equal(ha[op], hb[op])
+    assert ra == rb
+
+
+@pytest.mark.parametrize("mask", [ALL, 1 << sw2d.SW2D_RED_VOLUME,
+                                  (1 << sw2d.SW2D_RED_MAX_ABS_U) | (1 << sw2d.SW2D_RED_WET_COUNT)])
+def test_fused_per_step_reductions(mask):
+    """The fused epilogue's per-step diagnostics against the oracle's
+    per-step history (sums 1e-5 relative; max/min/count exact); fields stay
+    bitwise whatever the reduction level."""
+    cfg, st = _bowl(389, 277)
+    want = oracle_run(P, st, 40, history=True)
+    got, hist, _, _ = gpu_run(P, st, 40, reduce_mask=mask)
+    assert_state_equal(got, want[:4], where="with fused reductions")
+    ohist = want[4]
+    for op, series in hist.items():
+        for n in range(40):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[n]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = ohist[n, op]
+            check_reductions(row, ref)
+
+
+# --- virtual ranks: the multi-GPU decomposition on one device -------------
+
+@pytest.mark.parametrize("nranks", [2, 3, 5, 8])
+def test_virtual_ranks_bitwise_equal_single(nranks):
+    """Row slabs with a 2-row halo exchanged every step reproduce the
+    single-slab result bitwise (the per-cell arithmetic does not depend on
+    the slab), and the decomposed diagnostics agree."""
+    cfg, st = _bowl(263, 97)
+    one, h1, r1, _ = gpu_run(P, st, 80, reduce_mask=ALL)
+    many, hm, rm, _ = gpu_run(P, st, 80, reduce_mask=ALL,
+                              dist=sw2d.make_dist(0, nranks, virtual_ranks=1))
+    assert_state_equal(many, one, where=f"{nranks} virtual ranks")
+    want = oracle_run(P, st, 80)
+    assert_state_equal(many, want, where=f"{nranks} virtual ranks vs oracle")
+    check_reductions(rm, r1)
+
+
+# --- error contract --------------------------------------------------------
+
+def test_status_codes():
+    p = sw2d.make_params(16, 16)
+    h = sw2d.sw2d_create(p)
+    try:
+        with pytest.raises(sw2d.Sw2dError) as ei:
+            sw2d.sw2d_step(h, 1)
+        assert ei.value.code == sw2d.SW2D_ESTATE
+        with pytest.raises(sw2d.Sw2dError) as ei:
+            sw2d.sw2d_reduce(h, 0)
+        assert ei.value.code == sw2d.SW2D_ESTATE
+        hz = np.full((16, 16), 10.0, np.float32)
+        e = np.zeros_like(hz)
+        e[3, 4] = np.nan
+        with pytest.raises(sw2d.Sw2dError) as ei:
+            sw2d.sw2d_set_state(h, hz, e)
+        assert ei.value.code == sw2d.SW2D_EINVAL
+        e[3, 4] = 0.0
+        sw2d.sw2d_set_state(h, hz, e)          # recovers: EINVAL is not sticky
+        sw2d.sw2d_step(h, 3)
+        with pytest.raises(sw2d.Sw2dError) as ei:
+            sw2d.sw2d_reduce_history(h, 0, 1)  # op not in reduce_every_step
+        assert ei.value.code == sw2d.SW2D_EINVAL
+        with pytest.raises(sw2d.Sw2dError):
+            sw2d.sw2d_step(h, -1)
+    finally:
+        sw2d.sw2d_destroy(h)
+    with pytest.raises(sw2d.Sw2dError) as ei:
+        sw2d.sw2d_create(sw2d.make_params(16, 7), sw2d.make_dist(0, 2, virtual_ranks=1))
+    assert ei.value.code == sw2d.SW2D_EINVAL
+
+
+def test_wall_faces_ignored_on_input_and_zero_on_output():
+    cfg, st = _bowl(130, 60)
+    hz, e, u, v = [a.copy() for a in st]
+    u[:, -1] = 5.0     # east wall faces
+    v[-1, :] = -5.0    # north wall faces
+    got, _, _, _ = gpu_run(P, (hz, e, u, v), 0)
+    assert np.all(got[1][:, -1] == 0) and np.all(got[2][-1, :] == 0)
+    want = oracle_run(P, (hz, e, u, v), 10)
+    got, _, _, _ = gpu_run(P, (hz, e, u, v), 10)
+    assert_state_equal(got, want, where="wall faces on input")
+
+
+def test_torch_device_buffers():
+    """set/get state from CUDA tensors (UVA) equals the host path."""
+    import torch
+    cfg, st = _bowl(200, 150)
+    dev = [torch.from_numpy(a).cuda() for a in st]
+    p = sw2d.make_params(200, 150)
+    h = sw2d.sw2d_create(p, None, torch.cuda.current_stream())
+    try:
+        sw2d.sw2d_set_state(h, *dev)
+        sw2d.sw2d_step(h, 30)
+        out = [torch.empty_like(dev[0]) for _ in range(3)]
+        sw2d.sw2d_get_state(h, *out)
+        torch.cuda.synchronize()
+    finally:
+        sw2d.sw2d_destroy(h)
+    want = oracle_run(P, st, 30)
+    assert_state_equal([o.cpu().numpy() for o in out] + [None], want, where="torch buffers")
+
+
+# --- full BASELINE sizes: sampled windows + properties ---------------------
+
+def _window_parity(cfg, got, nsteps, centers, size=48):
+    """Oracle on windows of the initial state with a margin of 2*nsteps+2
+    cells (the step's dependency cone is 2 cells per step; cells farther than
+    that from a window edge that is not a real wall are exact)."""
+    nx, ny = cfg["nx"], cfg["ny"]
+    m = 2 * nsteps + 2
+    for (jc, kc) in centers:
+        j0 = min(max(jc - size // 2, 0), ny - size)
+        k0 = min(max(kc - size // 2, 0), nx - size)
+        wj0, wk0 = max(j0 - m, 0), max(k0 - m, 0)
+        wj1, wk1 = min(j0 + size + m, ny), min(k0 + size + m, nx)
+        st = si.generate(cfg, j0=wj0, nrows=wj1 - wj0, k0=wk0, ncols=wk1 - wk0)
+        want = oracle_run(P, st, nsteps)
+        sl = (slice(j0 - wj0, j0 - wj0 + size), slice(k0 - wk0, k0 - wk0 + size))
+        sub = [g[j0:j0 + size, k0:k0 + size] for g in got]
+        assert_state_equal(sub, [w[sl] for w in want],
+                           where=f"window at ({j0},{k0}) after {nsteps} steps")
+
+
+def _full_size_run(cfg, nsteps, mask):
+    nx, ny = cfg["nx"], cfg["ny"]
+    st = si.generate(cfg)
+    p = sw2d.make_params(nx, ny, reduce_every_step=mask, history_len=nsteps)
+    h = sw2d.sw2d_create(p)
+    try:
+        sw2d.sw2d_set_state(h, *st)
+        v0 = sw2d.sw2d_reduce(h, sw2d.SW2D_RED_VOLUME)
+        sw2d.sw2d_step(h, nsteps)
+        got = sw2d.get_state(h, nx)
+        hist = sw2d.sw2d_reduce_history(h, sw2d.SW2D_RED_VOLUME, nsteps) if mask else None
+        red = [sw2d.sw2d_reduce(h, op) for op in range(sw2d.SW2D_RED_N)]
+    finally:
+        sw2d.sw2d_destroy(h)
+    return st, got, v0, hist, red
+
+
+def _sample_centers(cfg, got):
+    nx, ny = cfg["nx"], cfg["ny"]
+    e = got[0]
+    # corners, edge midpoints, centre, the bump peak, a shoreline cell
+    w = got[3]
+    shore = np.argwhere(w[ny // 2, :-1] != w[ny // 2, 1:])
+    sk = int(shore[0][0]) if len(shore) else nx // 3
+    peak = np.unravel_index(np.argmax(np.abs(e)), e.shape)
+    return [(0, 0), (0, nx - 1), (ny - 1, 0), (ny - 1, nx - 1), (ny // 2, 0),
+            (0, nx // 2), (ny // 2, nx // 2), (int(peak[0]), int(peak[1])), (ny // 2, sk)]
+
+
+def test_c3_full_size_sampled_parity():
+    cfg = si.config("c3")
+    n = 100
+    st, got, v0, _, red = _full_size_run(cfg, n, 0)
+    _window_parity(cfg, got, n, _sample_centers(cfg, got))
+    assert abs(red[sw2d.SW2D_RED_VOLUME] - v0) <= 1e-6 * v0
+
+
+def test_c5_bench_configuration_sampled_parity():
+    """bench.py's launch configuration: C5 16384^2 on one GPU with the
+    per-step VOLUME reduction fused."""
+    cfg = si.config("c5", 1)
+    n = 30
+    st, got, v0, hist, red = _full_size_run(cfg, n, 1 << sw2d.SW2D_RED_VOLUME)
+    _window_parity(cfg, got, n, _sample_centers(cfg, got), size=32)
+    assert np.max(np.abs(hist - v0)) <= 1e-6 * v0
+    assert abs(hist[-1] - red[sw2d.SW2D_RED_VOLUME]) <= 1e-9 * v0
