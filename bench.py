@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4"], default="c5")
     ap.add_argument("--substeps", type=int, default=None,
                     help="model time steps per bench step (default 100; c2: 10000)")
+    ap.add_argument("--reduce", choices=["default", "none", "volume", "all"], default="default",
+                    help="per-step fused diagnostics (default: VOLUME for c5, none otherwise)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -198,7 +200,8 @@ def workload_config(cfg, args, ws):
         "workload": f"{cfg['name']}: {cfg['desc']}",
         "nx": cfg["nx"], "ny": cfg["ny"], "cells_per_gpu": cfg["nx"] * cfg["ny"] // ws,
         "substeps_per_step": args.substeps, "dx": cfg["dx"], "dt": cfg["dt"],
-        "reduce_every_step": "VOLUME" if cfg["name"] in ("c5",) else "none",
+        "reduce_every_step": args.reduce if args.reduce != "default" else
+        ("VOLUME" if cfg["name"] == "c5" else "none"),
         "parallelism": f"row slabs x{ws}" if ws > 1 else "1 GPU",
         "l2": "inputs larger than L2 (state >> 126 MB), no flush"
         if cfg["nx"] * cfg["ny"] // ws * BYTES_PER_CELL > 1e9 else
@@ -223,6 +226,9 @@ def run_ours(args, cfg, ws, rank, local):
     j0, nrows = sw2d.sw2d_partition(ny, ws, rank)
     T = args.substeps
     mask = (1 << sw2d.SW2D_RED_VOLUME) if cfg["name"] == "c5" else 0
+    if args.reduce != "default":
+        mask = {"none": 0, "volume": 1 << sw2d.SW2D_RED_VOLUME,
+                "all": (1 << sw2d.SW2D_RED_N) - 1}[args.reduce]
 
     # inputs for this rank's slab, in pinned host memory
     host = [torch.empty((nrows, nx), dtype=torch.float32, pin_memory=True) for _ in range(4)]
@@ -283,7 +289,7 @@ def run_ours(args, cfg, ws, rank, local):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
                 "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells_local,
-                "kernel": "sw2d_step_fused<1>" if mask else "sw2d_step_fused<0>",
+                "kernel": "sw2d_step_fused<%d>" % (0 if not mask else (1 if mask < 4 else 2)),
                 "launches_per_model_step": step_launches_per_model_step,
                 "peak_source": peak_src,
                 "note": "per-model-step time of the whole timed region (the step kernel "

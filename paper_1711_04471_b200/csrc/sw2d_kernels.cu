@@ -44,22 +44,6 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c,
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
 }
 
-// Upwind volume flux through a face with velocity s (reading R3):
-// s > 0 ? s*hL : (s < 0 ? s*hR : 0), both products formed, then selected.
-__device__ __forceinline__ float flux(float s, float hl, float hr) {
-  const float a = __fmul_rn(s, hl);
-  const float b = __fmul_rn(s, hr);
-  return s > 0.0f ? a : (s < 0.0f ? b : 0.0f);
-}
-
-// Wet/dry face rule of the momentum predictor (reading R4): returns the new
-// face velocity old + d if the face carries flow, else 0.
-__device__ __forceinline__ float face(bool wc, bool wn, float d, float old,
-                                      bool ok) {
-  const bool flow = wc ? (wn || d > 0.0f) : (wn && d < 0.0f);
-  return (ok && flow) ? __fadd_rn(old, d) : 0.0f;
-}
-
 struct Acc {
   double sum_eta;
   double wet;
@@ -173,12 +157,259 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
 
 // ---------------------------------------------------------------------------
 // The fused step.
+//
+// Per lane: 4 consecutive columns k0..k0+3 (one float4 of each field).  Wet
+// flags travel as bit masks (bit c = column k0+c) so one shuffle moves a
+// lane's four flags.  The Shapiro filter of row r is split in two halves:
+// when etan(r) is known (iteration r+1) the part that needs rows r-1 and r
+// is formed, A = t1 + t2 and sS = sel(wS, etan(r-1)); when etan(r+1) is known
+// (iteration r+2) the north term completes E'(r) = A + q*(sel(wN, etan(r+1))
+// + sS) — the same operations, in the same order, as the sequential scheme
+// (fadd is commutative), so the window is two rows deep everywhere.
 // ---------------------------------------------------------------------------
+
+// rolling window carried from row L-1 into row L
+struct Win {
+  float e[4];      // eta(L-1)
+  float h[4];      // h(L-1)
+  float un[4];     // un(L-1)
+  float v[4];      // V(L-1), old
+  float fy[4];     // y-flux through the north face of row L-2
+  float A[4];      // Shapiro of row L-2: t1 + t2
+  float sS[4];     // Shapiro of row L-2: sel(wS, etan(L-3))
+  float etC[4];    // etan(L-2)
+  float h0P[4];    // hzero(L-1)   (diagnostics level 2)
+  float h0PP[4];   // hzero(L-2)   (diagnostics level 2)
+  float hR;        // h(L-1, k0+4)
+  unsigned wext;   // wet bits of row L-1: bit c+1 = column k0+c, c = -1..4
+  unsigned wPP;    // wet bits of row L-2: bit c = column k0+c
+};
+
+struct Ctx {
+  float cgx, cgy, cx, cy, q, hmin;
+  unsigned colmask;  // columns 1..nx of this lane's four
+  unsigned umask;    // columns 1..nx-1 (faces that are not the east wall)
+  int ny, ra, rb;    // global rows (1-based): grid rows, this segment's output rows
+  bool out_lane;
+};
+
+// the four byte-lanes of the result hold bits 0..3 of m (m < 16)
+__device__ __forceinline__ unsigned spread4(unsigned m) {
+  return (m * 0x00204081u) & 0x01010101u;
+}
+
+__device__ __forceinline__ bool bit(unsigned m, int i) { return (m >> i) & 1u; }
+
+// rows r with lo <= r <= hi (requires lo <= hi)
+__device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
+  return (unsigned)(r - lo) <= (unsigned)(hi - lo);
+}
+
+// Upwind flux s > 0 ? s*hL : (s < 0 ? s*hR : 0) as s * (s > 0 ? hL : hR):
+// equal in value for finite depths (s = 0 gives a zero either way).
+__device__ __forceinline__ float flux(float s, float hl, float hr) {
+  return __fmul_rn(s, s > 0.0f ? hl : hr);
+}
+
+// Wet/dry face rule (reading R4): the face between a cell with wet flag wc
+// and its east/north neighbour (wn) carries flow iff
+// wc ? (wn || d > 0) : (wn && d < 0); a blocked face gets 0.
+__device__ __forceinline__ float face(bool wc, bool wn, float d, float old) {
+  const bool flow = (wc & (wn | (d > 0.0f))) | (wn & (d < 0.0f));
+  return flow ? __fadd_rn(old, d) : 0.0f;
+}
+
+// One loaded row L: reads the window `w` (rows L-1, L-2), writes `o`.
+template <int RED>
+__device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
+                                         const float4 H4, const float4 U4,
+                                         const float4 V4, const int L, const Ctx& x,
+                                         Acc& acc, float* pU, float* pV, float* pE) {
+  const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
+  const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
+  const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
+  const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+
+  // a1: h and wet flags of row L (rows outside 1..ny and columns outside
+  // 1..nx are dry)
+  float hL[4];
+  unsigned wL = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    hL[c] = __fadd_rn(h0L[c], eL[c]);
+    wL |= (hL[c] < x.hmin) ? 0u : (1u << c);
+  }
+  wL &= in_rows(L, 1, x.ny) ? x.colmask : 0u;
+  const float eR = __shfl_down_sync(kFull, eL[0], 1);
+  const float hR = __shfl_down_sync(kFull, hL[0], 1);
+  const unsigned wRb = __shfl_down_sync(kFull, wL, 1);
+  const unsigned wLb = __shfl_up_sync(kFull, wL, 1);
+  const unsigned wext = ((wLb >> 3) & 1u) | (wL << 1) | ((wRb & 1u) << 5);
+
+  // a2: un(L) on the east faces of row L; vn(L-1) on the north faces of L-1
+  const unsigned wP = (w.wext >> 1) & 15u;
+  const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north wall
+  float un[4], vn[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float en = (c < 3) ? eL[c + 1] : eR;
+    const float du = __fmul_rn(x.cgx, __fsub_rn(en, eL[c]));
+    const float u = face(bit(wext, c + 1), bit(wext, c + 2), du, uL[c]);
+    un[c] = bit(x.umask, c) ? u : 0.0f;
+    const float dv = __fmul_rn(x.cgy, __fsub_rn(eL[c], w.e[c]));
+    const float v = face(bit(wP, c), bit(wL, c), dv, w.v[c]);
+    vn[c] = vrow ? v : 0.0f;
+  }
+
+  // a3: fluxes of row L-1 and etan(L-1)
+  float fx[4], fy[4], et[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    fx[c] = flux(w.un[c], w.h[c], (c < 3) ? w.h[c + 1] : w.hR);
+    fy[c] = flux(vn[c], w.h[c], hL[c]);
+  }
+  const float fxw = __shfl_up_sync(kFull, fx[3], 1);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float fw = (c > 0) ? fx[c - 1] : fxw;
+    et[c] = __fsub_rn(__fsub_rn(w.e[c], __fmul_rn(x.cx, __fsub_rn(fx[c], fw))),
+                      __fmul_rn(x.cy, __fsub_rn(fy[c], w.fy[c])));
+  }
+
+  // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
+  float En[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float t3 = __fmul_rn(x.q, __fadd_rn(bit(wP, c) ? et[c] : 0.0f, w.sS[c]));
+    En[c] = bit(w.wPP, c) ? __fadd_rn(w.A[c], t3) : w.etC[c];
+  }
+
+  // a4 (first half) for row L-1: s, t1, t2, sS
+  const float etW = __shfl_up_sync(kFull, et[3], 1);
+  const float etE = __shfl_down_sync(kFull, et[0], 1);
+  const unsigned cnt = spread4((w.wext >> 2) & 15u) + spread4(w.wext & 15u) +
+                       spread4(wL) + spread4(w.wPP);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float s = (float)((cnt >> (8 * c)) & 0xffu);
+    const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(x.q, s)), et[c]);
+    const float xE = bit(w.wext, c + 2) ? ((c < 3) ? et[c + 1] : etE) : 0.0f;
+    const float xW = bit(w.wext, c) ? ((c > 0) ? et[c - 1] : etW) : 0.0f;
+    o.A[c] = __fadd_rn(t1, __fmul_rn(x.q, __fadd_rn(xE, xW)));
+    o.sS[c] = bit(w.wPP, c) ? w.etC[c] : 0.0f;
+  }
+
+  // a5: commit (lanes 1..30, rows of this segment)
+  if (x.out_lane) {
+    if (in_rows(L, x.ra, x.rb)) {
+      st4(pU, un[0], un[1], un[2], un[3]);
+      if (RED >= 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(un[c]));
+      }
+    }
+    if (in_rows(L - 1, x.ra, x.rb)) {
+      st4(pV, vn[0], vn[1], vn[2], vn[3]);
+      if (RED >= 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vn[c]));
+      }
+    }
+    if (in_rows(L - 2, x.ra, x.rb)) {
+      st4(pE, En[0], En[1], En[2], En[3]);
+      if (RED >= 1) {
+        // columns outside 1..nx hold exactly 0 (their etan is 0)
+        acc.sum_eta += ((double)En[0] + (double)En[1]) + ((double)En[2] + (double)En[3]);
+      }
+      if (RED >= 2) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (bit(x.colmask, c)) {
+            acc.max_eta = fmaxf(acc.max_eta, En[c]);
+            acc.neg_min_eta = fmaxf(acc.neg_min_eta, -En[c]);
+            acc.wet += (__fadd_rn(w.h0PP[c], En[c]) < x.hmin) ? 0.0 : 1.0;
+          }
+        }
+      }
+    }
+  }
+
+  // the window for row L+1
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    o.e[c] = eL[c];
+    o.h[c] = hL[c];
+    o.un[c] = un[c];
+    o.v[c] = vL[c];
+    o.fy[c] = fy[c];
+    o.etC[c] = et[c];
+    if (RED >= 2) {
+      o.h0PP[c] = w.h0P[c];
+      o.h0P[c] = h0L[c];
+    }
+  }
+  o.hR = hR;
+  o.wPP = wP;
+  o.wext = wext;
+}
+
+// --- TMA bulk-copy row ring (one per warp) ---------------------------------
+// Each warp streams its strip through a ring of kStages shared-memory stages;
+// a stage holds one row of the four input fields (4 x 512 B), filled by
+// cp.async.bulk (TMA) issued by lane 0 kStages-1 rows ahead and completed on
+// the stage's mbarrier (complete_tx).  The loads therefore need no registers
+// and several rows per warp are in flight.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const float* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int kStages = 4;                        // rows in flight per warp
+constexpr int kRowBytes = 32 * 16;                // one field, one row, one strip
+constexpr int kStageBytes = 4 * kRowBytes;        // E, H0, U, V
+constexpr int kSmemPerWarp = kStages * kStageBytes;
+
 template <int RED>
 __global__ void __launch_bounds__(kThreads)
     sw2d_step_fused(const StepArgs a) {
+  __shared__ __align__(128) unsigned char ring[kWarpsPerBlock][kSmemPerWarp];
+  __shared__ __align__(8) unsigned long long bars[kWarpsPerBlock][kStages];
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * kWarpsPerBlock + warp;
   const int strip = gw % a.nstrips;
   const int seg = gw / a.nstrips;
 
@@ -186,172 +417,117 @@ __global__ void __launch_bounds__(kThreads)
   acc.init();
 
   if (seg < a.nsegs) {  // warp-uniform
-    const long long ra = a.row_lo + (long long)seg * a.rows_per_seg;
-    const long long rb = min(a.row_hi, ra + a.rows_per_seg - 1);
+    Ctx x;
+    x.ra = (int)a.row_lo + seg * a.rows_per_seg;
+    x.rb = min((int)a.row_hi, x.ra + a.rows_per_seg - 1);
     const int c0 = strip * kColsPerStrip + lane * 4;  // storage column of element 0
     const int k0 = c0 - kColOff;                      // its 1-based column
-    const int nx = a.nx;
-    const long long ny = a.ny;
-    const bool out_lane = (lane >= 1) && (lane <= kOutLanes);
-    bool colok[4], uok[4];
+    x.colmask = 0;
+    x.umask = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      colok[c] = (k0 + c >= 1) && (k0 + c <= nx);
-      uok[c] = (k0 + c >= 1) && (k0 + c <= nx - 1);
+      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
     }
-    const float cgx = a.c.cgx, cgy = a.c.cgy, cx = a.c.cx, cy = a.c.cy;
-    const float q = a.c.q, hmin = a.c.hmin;
+    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    x.q = a.c.q; x.hmin = a.c.hmin;
+    x.ny = (int)a.ny;
+    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
     const long long pitch = a.s.pitch;
 
-    // rolling window (rows relative to the loaded row L)
-    float eP[4] = {0.f, 0.f, 0.f, 0.f};    // eta(L-1)
-    float hP[4] = {0.f, 0.f, 0.f, 0.f};    // h(L-1)
-    float unP[4] = {0.f, 0.f, 0.f, 0.f};   // un(L-1)
-    float vP[4] = {0.f, 0.f, 0.f, 0.f};    // V(L-1) (old)
-    float fyP[4] = {0.f, 0.f, 0.f, 0.f};   // y-flux through the north face of row L-2
-    float etP[4] = {0.f, 0.f, 0.f, 0.f};   // etan(L-2)
-    float etPP[4] = {0.f, 0.f, 0.f, 0.f};  // etan(L-3)
-    float h0P[4] = {0.f, 0.f, 0.f, 0.f};   // hzero(L-1)  (RED >= 2)
-    float h0PP[4] = {0.f, 0.f, 0.f, 0.f};  // hzero(L-2)  (RED >= 2)
-    float hRP = 0.f;                       // h(L-1, k0+4)
-    unsigned wP = 0, wPP = 0, wPPP = 0;    // wet bits of rows L-1, L-2, L-3
+    const int first = x.ra - 2;      // first loaded row
+    const int last = x.rb + 2;       // last loaded row
+    // element offset of (row `first`, strip column 0) from each field's base
+    const long long off0 = (long long)(first - (int)a.s.jbase) * pitch + strip * kColsPerStrip;
+    const uint32_t sbase = smem_u32(&ring[warp][0]);
+    const uint32_t bbase = smem_u32(&bars[warp][0]);
 
-    long long L = ra - 2;
-    const long long last = rb + 2;
-    long long off = (L - a.s.jbase) * pitch + c0;
-    float4 nE = ldg4(a.s.E + off), nH = ldg4(a.s.H0 + off);
-    float4 nU = ldg4(a.s.U + off), nV = ldg4(a.s.V + off);
-
-    for (; L <= last; ++L) {
-      const float eL[4] = {nE.x, nE.y, nE.z, nE.w};
-      const float h0L[4] = {nH.x, nH.y, nH.z, nH.w};
-      const float uL[4] = {nU.x, nU.y, nU.z, nU.w};
-      const float vL[4] = {nV.x, nV.y, nV.z, nV.w};
-      const long long cur = off;
-      if (L < last) off += pitch;  // prefetch the next row (re-load the last one)
-      nE = ldg4(a.s.E + off);
-      nH = ldg4(a.s.H0 + off);
-      nU = ldg4(a.s.U + off);
-      nV = ldg4(a.s.V + off);
-
-      // a1: h and wet of row L
-      const bool rowok = (L >= 1) && (L <= ny);
-      float hL[4];
-      unsigned wL = 0;
+    // lane 0: initialise the ring and issue rows first .. first+kStages-1
+    if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        hL[c] = __fadd_rn(h0L[c], eL[c]);
-        wL |= (rowok && colok[c] && !(hL[c] < hmin)) ? (1u << c) : 0u;
-      }
-      const float eR = __shfl_down_sync(kFull, eL[0], 1);
-      const float hR = __shfl_down_sync(kFull, hL[0], 1);
-      const unsigned wRb = __shfl_down_sync(kFull, wL, 1);
-
-      // a2: un(L) (east faces) and vn(L-1) (north faces of row L-1)
-      float unL[4], vnP[4];
-      const bool vrow = (L - 1 >= 1) && (L - 1 <= ny - 1);
+      for (int st = 0; st < kStages; ++st) mbar_init(bbase + 8 * st, 1);
+      fence_proxy_async();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float en = (c < 3) ? eL[c + 1] : eR;
-        const bool wn = (c < 3) ? ((wL >> (c + 1)) & 1u) : (wRb & 1u);
-        const float du = __fmul_rn(cgx, __fsub_rn(en, eL[c]));
-        unL[c] = face((wL >> c) & 1u, wn, du, uL[c], rowok && uok[c]);
-        const float dv = __fmul_rn(cgy, __fsub_rn(eL[c], eP[c]));
-        vnP[c] = face((wP >> c) & 1u, (wL >> c) & 1u, dv, vP[c],
-                      vrow && colok[c]);
-      }
-
-      // a3: fluxes and etan(L-1)
-      float fx[4], fy[4], et[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float hr = (c < 3) ? hP[c + 1] : hRP;
-        fx[c] = flux(unP[c], hP[c], hr);
-        fy[c] = flux(vnP[c], hP[c], hL[c]);
-      }
-      const float fxw = __shfl_up_sync(kFull, fx[3], 1);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const float fw = (c > 0) ? fx[c - 1] : fxw;
-        et[c] = __fsub_rn(__fsub_rn(eP[c], __fmul_rn(cx, __fsub_rn(fx[c], fw))),
-                          __fmul_rn(cy, __fsub_rn(fy[c], fyP[c])));
-      }
-
-      // a4: Shapiro filter of row L-2 (centre etP, north et, south etPP)
-      const float etW = __shfl_up_sync(kFull, etP[3], 1);
-      const float etE = __shfl_down_sync(kFull, etP[0], 1);
-      const unsigned wWb = __shfl_up_sync(kFull, wPP, 1);
-      const unsigned wEb = __shfl_down_sync(kFull, wPP, 1);
-      float En[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const unsigned wE = (c < 3) ? ((wPP >> (c + 1)) & 1u) : (wEb & 1u);
-        const unsigned wW = (c > 0) ? ((wPP >> (c - 1)) & 1u) : ((wWb >> 3) & 1u);
-        const unsigned wN = (wP >> c) & 1u;
-        const unsigned wS = (wPPP >> c) & 1u;
-        const float xE = (c < 3) ? etP[c + 1] : etE;
-        const float xW = (c > 0) ? etP[c - 1] : etW;
-        const float s = (float)(int)(wE + wW + wN + wS);
-        const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(q, s)), etP[c]);
-        const float t2 = __fmul_rn(q, __fadd_rn(wE ? xE : 0.0f, wW ? xW : 0.0f));
-        const float t3 = __fmul_rn(q, __fadd_rn(wN ? et[c] : 0.0f, wS ? etPP[c] : 0.0f));
-        const float f = ((wPP >> c) & 1u) ? __fadd_rn(__fadd_rn(t1, t2), t3) : etP[c];
-        En[c] = colok[c] ? f : 0.0f;
-      }
-
-      // a5: commit (lanes 1..30; rows of this segment only)
-      if (out_lane) {
-        if (L >= ra && L <= rb) {
-          st4(a.s.Un + cur, unL[0], unL[1], unL[2], unL[3]);
-          if (RED >= 2) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(unL[c]));
-          }
-        }
-        if (L - 1 >= ra && L - 1 <= rb) {
-          st4(a.s.Vn + cur - pitch, vnP[0], vnP[1], vnP[2], vnP[3]);
-          if (RED >= 2) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vnP[c]));
-          }
-        }
-        if (L - 2 >= ra && L - 2 <= rb) {
-          st4(a.s.En + cur - 2 * pitch, En[0], En[1], En[2], En[3]);
-          if (RED >= 1) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              if (colok[c]) {
-                acc.sum_eta += (double)En[c];
-                if (RED >= 2) {
-                  acc.max_eta = fmaxf(acc.max_eta, En[c]);
-                  acc.neg_min_eta = fmaxf(acc.neg_min_eta, -En[c]);
-                  acc.wet += (__fadd_rn(h0PP[c], En[c]) < hmin) ? 0.0 : 1.0;
-                }
-              }
-            }
-          }
+      for (int st = 0; st < kStages; ++st) {
+        if (first + st <= last) {
+          const long long o = off0 + st * pitch;
+          const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
+          mbar_expect_tx(b, kStageBytes);
+          bulk_g2s(d, a.s.E + o, kRowBytes, b);
+          bulk_g2s(d + kRowBytes, a.s.H0 + o, kRowBytes, b);
+          bulk_g2s(d + 2 * kRowBytes, a.s.U + o, kRowBytes, b);
+          bulk_g2s(d + 3 * kRowBytes, a.s.V + o, kRowBytes, b);
         }
       }
+    }
+    __syncwarp();
 
-      // rotate the window
+    Win wa, wb;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        etPP[c] = etP[c];
-        etP[c] = et[c];
-        eP[c] = eL[c];
-        hP[c] = hL[c];
-        unP[c] = unL[c];
-        vP[c] = vL[c];
-        fyP[c] = fy[c];
-        if (RED >= 2) {
-          h0PP[c] = h0P[c];
-          h0P[c] = h0L[c];
-        }
+    for (int c = 0; c < 4; ++c) {
+      wa.e[c] = wa.h[c] = wa.un[c] = wa.v[c] = wa.fy[c] = 0.0f;
+      wa.A[c] = wa.sS[c] = wa.etC[c] = wa.h0P[c] = wa.h0PP[c] = 0.0f;
+    }
+    wa.hR = 0.0f;
+    wa.wext = 0;
+    wa.wPP = 0;
+
+    float* __restrict__ En = a.s.En;
+    float* __restrict__ Un = a.s.Un;
+    float* __restrict__ Vn = a.s.Vn;
+    const long long lo = off0 + lane * 4;   // this lane's element offset, row `first`
+
+    // consume row `first + i` from stage i % kStages; refill it with row
+    // first + i + kStages
+    auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
+      const int st = i & (kStages - 1);
+      const uint32_t b = bbase + 8 * st;
+      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
+      while (!mbar_try_wait(b, ph)) {
       }
-      hRP = hR;
-      wPPP = wPP;
-      wPP = wP;
-      wP = wL;
+      const float4* s4 = reinterpret_cast<const float4*>(&ring[warp][st * kStageBytes]) + lane;
+      E4 = s4[0];
+      H4 = s4[32];
+      U4 = s4[64];
+      V4 = s4[96];
+    };
+    auto refill = [&](int i) {
+      __syncwarp();
+      const int r = first + i + kStages;
+      if (lane == 0 && r <= last) {
+        const int st = i & (kStages - 1);
+        const long long o = off0 + (long long)(i + kStages) * pitch;
+        const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
+        fence_proxy_async();
+        mbar_expect_tx(b, kStageBytes);
+        bulk_g2s(d, a.s.E + o, kRowBytes, b);
+        bulk_g2s(d + kRowBytes, a.s.H0 + o, kRowBytes, b);
+        bulk_g2s(d + 2 * kRowBytes, a.s.U + o, kRowBytes, b);
+        bulk_g2s(d + 3 * kRowBytes, a.s.V + o, kRowBytes, b);
+      }
+    };
+
+    const int n = last - first + 1;
+    int i = 0;
+    // two rows per trip: the window ping-pongs between wa and wb
+    for (; i + 1 < n; i += 2) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)i * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+                    En + o - 2 * pitch);
+      refill(i);
+      fetch(i + 1, E4, H4, U4, V4);
+      row_step<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
+                    En + o - pitch);
+      refill(i + 1);
+    }
+    if (i < n) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)i * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+                    En + o - 2 * pitch);
     }
   }
   if (RED >= 1) block_reduce_and_finalize<RED>(acc, a.red);
