@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,6 +55,7 @@ struct sw2d {
   int64_t pitch = 0;
   int nstrips = 0;
   int red_level = 0;
+  int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
   std::vector<Slab> slabs;
   std::vector<Launch> launches;
   int step_blocks = 0;
@@ -164,9 +166,11 @@ float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch;
 void plan_launches(sw2d* h) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  const int bps = step_occupancy_blocks_per_sm(h->red_level);
-  const long long resident_warps = (long long)sms * bps * kWarpsPerBlock;
-  const long long target_segs = std::max(1LL, resident_warps / h->nstrips);
+  const int bps = step_occupancy_blocks_per_sm(h->red_level, h->kind);
+  // one wave: resident CTAs / CTAs across the columns
+  const int per = step_strips_per_cta(h->kind);
+  const long long ncc = (h->nstrips + per - 1) / per;
+  const long long target_segs = std::max(1LL, (long long)sms * bps / ncc);
   h->launches.clear();
   int part = 0;
   auto add = [&](int s, long long lo, long long hi, int phase) {
@@ -181,8 +185,7 @@ void plan_launches(sw2d* h) {
     L.rows_per_seg = (int)rps;
     L.nsegs = (int)((rows + rps - 1) / rps);
     L.phase = phase;
-    const long long warps = (long long)L.nsegs * h->nstrips;
-    L.blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    L.blocks = step_grid(h->kind, h->nstrips, L.nsegs);
     L.part_base = part;
     part += L.blocks;
     h->launches.push_back(L);
@@ -338,6 +341,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   h->p = *params;
   if (h->p.history_len == 0) h->p.history_len = kDefaultHistory;
   h->coef = make_coef(h->p);
+  if (const char* k = std::getenv("SW2D_STEP_KERNEL")) h->kind = std::atoi(k) == 0 ? 0 : 1;
   h->red_level = red_level_of(h->p.reduce_every_step);
   h->hist_len = h->p.history_len;
   if (dist) {
@@ -365,7 +369,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     h->slabs.push_back(s);
   }
   h->nstrips = (int)((h->p.nx + kColsPerStrip - 1) / kColsPerStrip);
-  const int64_t need = (int64_t)h->nstrips * kColsPerStrip + 8;
+  const int64_t need = (int64_t)h->nstrips * kColsPerStrip + kStripBase + 8;
   h->pitch = (need + 31) / 32 * 32;
   // streams
   if (cuda_stream) {
@@ -589,7 +593,7 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
           CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
           waited = true;
         }
-        launch_step(step_args(h, L, rec), h->red_level, h->stream);
+        launch_step(step_args(h, L, rec), h->red_level, h->kind, h->stream);
         h->nlaunch++;
       }
     }

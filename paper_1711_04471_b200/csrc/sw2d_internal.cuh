@@ -5,17 +5,23 @@
 // row-major float32 array of (nrows + 4) rows x `pitch` floats.  Storage row
 // r holds global 1-based row j = jbase + r (jbase = first owned row - 2, so
 // two halo rows sit on each side).  Storage column c holds 1-based interior
-// column k = c - kColOff (k = 1 at c = 4: 16-byte aligned; the west wall
-// halo column k = 0 is c = 3).  pitch is a multiple of 32 floats (128 B).
+// column k = c - kColOff (k = 1 at c = 8; the west wall halo column k = 0 is
+// c = 7).  Warp strip s reads storage columns [120 s + 4, 120 s + 132) and
+// writes [120 s + 8, 120 s + 128): 15 whole 32-byte sectors, so no sector is
+// written by two warps.  pitch is a multiple of 32 floats (128 B).
 #pragma once
 #include <cstdint>
 
 namespace sw2d_dev {
 
-constexpr int kColOff = 3;           // storage column of 1-based column k is k + 3
+constexpr int kColOff = 7;           // storage column of 1-based column k is k + 7
+constexpr int kStripBase = kColOff - 3;  // storage column where strip 0's window starts
 constexpr int kHaloRows = 2;         // halo rows per side (the fused step's cone)
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 4;      // grid-stride helper kernels
 constexpr int kThreads = 32 * kWarpsPerBlock;
+constexpr int kStepWarps = 1;          // step kernel: one warp per CTA (its strip
+                                       // and segment are CTA-uniform, so TMA
+                                       // operands live in uniform registers)
 constexpr int kOutLanes = 30;        // lanes 1..30 produce output; 0 and 31 are halo lanes
 constexpr int kColsPerStrip = 4 * kOutLanes;   // 120 output columns per warp strip
 
@@ -72,11 +78,14 @@ struct StepArgs {
   RedArgs red;
 };
 
-// Kernel launchers (sw2d_kernels.cu).  `red_level`: 0 none, 1 sums
-// (VOLUME, SUM_ETA), 2 all diagnostics.
-int step_blocks(const StepArgs& a);
-void launch_step(const StepArgs& a, int red_level, void* stream);
-int step_occupancy_blocks_per_sm(int red_level);
+// Step-kernel launchers (sw2d_kernels.cu).  `red_level`: 0 none, 1 sums
+// (VOLUME, SUM_ETA), 2 all diagnostics.  `kind`: 0 = one warp per CTA with
+// its own TMA row ring; 1 = CTA of kCtaStrips compute warps + a producer warp
+// sharing one TMA row ring (default).
+int step_strips_per_cta(int kind);
+int step_grid(int kind, int nstrips, int nsegs);   // CTAs of one step launch
+void launch_step(const StepArgs& a, int red_level, int kind, void* stream);
+int step_occupancy_blocks_per_sm(int red_level, int kind);
 
 // set_state helper: checks finiteness of the interior, zeroes the wall faces
 // of U (k = nx) and V (global j = ny), and sums hzero in fp64 into *h0sum.

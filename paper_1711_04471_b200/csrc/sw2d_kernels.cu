@@ -65,9 +65,9 @@ __device__ __forceinline__ double shfl_xor_d(double x, int m) {
 // Block reduction of Acc -> one partial per CTA, then the last CTA of the
 // step (over all launches sharing the counter) folds the partials in a fixed
 // order (deterministic) and writes the 7-double record.
-template <int LEVEL>
+template <int LEVEL, int NW>
 __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
-  __shared__ Acc sh[kWarpsPerBlock];
+  __shared__ Acc sh[NW];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -86,7 +86,7 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
   __syncthreads();
   if (threadIdx.x == 0) {
     Acc t = sh[0];
-    for (int w = 1; w < kWarpsPerBlock; ++w) {
+    for (int w = 1; w < NW; ++w) {
       t.sum_eta += sh[w].sum_eta;
       t.wet += sh[w].wet;
       t.max_eta = fmaxf(t.max_eta, sh[w].max_eta);
@@ -113,7 +113,7 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
   // fixed tree over threads.
   Acc t;
   t.init();
-  for (int i = threadIdx.x; i < r.expected; i += kThreads) {
+  for (int i = threadIdx.x; i < r.expected; i += 32 * NW) {
     const volatile RedPartial* p = r.partials + i;
     t.sum_eta += p->sum_eta;
     t.wet += p->wet;
@@ -136,7 +136,7 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
   __syncthreads();
   if (threadIdx.x == 0) {
     Acc f = sh[0];
-    for (int w = 1; w < kWarpsPerBlock; ++w) {
+    for (int w = 1; w < NW; ++w) {
       f.sum_eta += sh[w].sum_eta;
       f.wet += sh[w].wet;
       f.max_eta = fmaxf(f.max_eta, sh[w].max_eta);
@@ -403,13 +403,13 @@ constexpr int kStageBytes = 4 * kRowBytes;        // E, H0, U, V
 constexpr int kSmemPerWarp = kStages * kStageBytes;
 
 template <int RED>
-__global__ void __launch_bounds__(kThreads)
-    sw2d_step_fused(const StepArgs a) {
-  __shared__ __align__(128) unsigned char ring[kWarpsPerBlock][kSmemPerWarp];
-  __shared__ __align__(8) unsigned long long bars[kWarpsPerBlock][kStages];
+__global__ void __launch_bounds__(32 * kStepWarps)
+    sw2d_step_warp(const StepArgs a) {
+  __shared__ __align__(128) unsigned char ring[kStepWarps][kSmemPerWarp];
+  __shared__ __align__(8) unsigned long long bars[kStepWarps][kStages];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int gw = blockIdx.x * kWarpsPerBlock + warp;
+  const int warp = kStepWarps == 1 ? 0 : (threadIdx.x >> 5);
+  const int gw = blockIdx.x * kStepWarps + warp;
   const int strip = gw % a.nstrips;
   const int seg = gw / a.nstrips;
 
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads)
     Ctx x;
     x.ra = (int)a.row_lo + seg * a.rows_per_seg;
     x.rb = min((int)a.row_hi, x.ra + a.rows_per_seg - 1);
-    const int c0 = strip * kColsPerStrip + lane * 4;  // storage column of element 0
+    const int c0 = strip * kColsPerStrip + kStripBase + lane * 4;  // storage column of element 0
     const int k0 = c0 - kColOff;                      // its 1-based column
     x.colmask = 0;
     x.umask = 0;
@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(kThreads)
     const int first = x.ra - 2;      // first loaded row
     const int last = x.rb + 2;       // last loaded row
     // element offset of (row `first`, strip column 0) from each field's base
-    const long long off0 = (long long)(first - (int)a.s.jbase) * pitch + strip * kColsPerStrip;
+    const long long off0 =
+        (long long)(first - (int)a.s.jbase) * pitch + strip * kColsPerStrip + kStripBase;
     const uint32_t sbase = smem_u32(&ring[warp][0]);
     const uint32_t bbase = smem_u32(&bars[warp][0]);
 
@@ -530,7 +531,153 @@ __global__ void __launch_bounds__(kThreads)
                     En + o - 2 * pitch);
     }
   }
-  if (RED >= 1) block_reduce_and_finalize<RED>(acc, a.red);
+  if (RED >= 1) block_reduce_and_finalize<RED, kStepWarps>(acc, a.red);
+}
+
+// --- CTA-shared row ring with a producer warp (kind 1, the default) --------
+// A CTA owns kCtaStrips adjacent warp strips of one row segment.  Warp
+// kCtaStrips is the producer: it streams one contiguous window of
+// 120 * (active strips) + 8 columns per field and row (the strips' 8-column
+// halo overlaps are fetched once per CTA) through a ring of kCtaStages
+// stages with cp.async.bulk (TMA), one full/empty mbarrier pair per stage.
+// The compute warps wait on `full`, copy their float4 of each field out of
+// the stage and release it on `empty` (one arrival per compute warp).
+constexpr int kCtaStrips = 8;
+constexpr int kCtaStages = 6;
+constexpr int kCtaWinBytes = (kCtaStrips * kColsPerStrip + 8) * 4;   // one field, one row
+constexpr int kCtaStageBytes = 4 * kCtaWinBytes;
+constexpr int kCtaThreads = 32 * (kCtaStrips + 1);
+constexpr int kCtaSmem = kCtaStages * kCtaStageBytes + 2 * 8 * kCtaStages;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int RED>
+__global__ void __launch_bounds__(kCtaThreads)
+    sw2d_step_cta(const StepArgs a) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  unsigned char* ring = dsm;
+  const uint32_t sring = smem_u32(ring);
+  const uint32_t sfull = sring + kCtaStages * kCtaStageBytes;
+  const uint32_t sempty = sfull + 8 * kCtaStages;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int ncc = (a.nstrips + kCtaStrips - 1) / kCtaStrips;
+  const int cc = blockIdx.x % ncc;
+  const int seg = blockIdx.x / ncc;
+  const int strip0 = cc * kCtaStrips;
+  const int nact = min(kCtaStrips, a.nstrips - strip0);   // active compute warps
+
+  Acc acc;
+  acc.init();
+
+  const int ra = (int)a.row_lo + seg * a.rows_per_seg;
+  const int rb = min((int)a.row_hi, ra + a.rows_per_seg - 1);
+  const int first = ra - 2;        // first loaded row
+  const int n = rb + 2 - first + 1; // rows streamed
+  const long long pitch = a.s.pitch;
+  const long long off0 =
+      (long long)(first - (int)a.s.jbase) * pitch + strip0 * kColsPerStrip + kStripBase;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < kCtaStages; ++st) {
+      mbar_init(sfull + 8 * st, 1);
+      mbar_init(sempty + 8 * st, nact);
+    }
+    fence_proxy_async();
+  }
+  __syncthreads();
+
+  if (warp == kCtaStrips) {
+    // producer warp: one elected lane streams the rows
+    if (lane == 0) {
+      const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
+      for (int r = 0; r < n; ++r) {
+        const int st = r % kCtaStages;
+        if (r >= kCtaStages) {
+          const uint32_t ph = (uint32_t)(r / kCtaStages - 1) & 1u;
+          while (!mbar_try_wait(sempty + 8 * st, ph)) {
+          }
+        }
+        const long long o = off0 + (long long)r * pitch;
+        const uint32_t d = sring + st * kCtaStageBytes, b = sfull + 8 * st;
+        mbar_expect_tx(b, 4u * wb);
+        bulk_g2s(d, a.s.E + o, wb, b);
+        bulk_g2s(d + kCtaWinBytes, a.s.H0 + o, wb, b);
+        bulk_g2s(d + 2 * kCtaWinBytes, a.s.U + o, wb, b);
+        bulk_g2s(d + 3 * kCtaWinBytes, a.s.V + o, wb, b);
+      }
+    }
+  } else if (warp < nact) {
+    Ctx x;
+    x.ra = ra;
+    x.rb = rb;
+    const int c0 = (strip0 + warp) * kColsPerStrip + kStripBase + lane * 4;
+    const int k0 = c0 - kColOff;
+    x.colmask = 0;
+    x.umask = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    x.q = a.c.q; x.hmin = a.c.hmin;
+    x.ny = (int)a.ny;
+    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+
+    Win wa, wb;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      wa.e[c] = wa.h[c] = wa.un[c] = wa.v[c] = wa.fy[c] = 0.0f;
+      wa.A[c] = wa.sS[c] = wa.etC[c] = wa.h0P[c] = wa.h0PP[c] = 0.0f;
+    }
+    wa.hR = 0.0f;
+    wa.wext = 0;
+    wa.wPP = 0;
+
+    float* __restrict__ En = a.s.En;
+    float* __restrict__ Un = a.s.Un;
+    float* __restrict__ Vn = a.s.Vn;
+    const long long lo = off0 + warp * kColsPerStrip + lane * 4;
+    const int sl = (warp * kColsPerStrip + lane * 4) * 4;
+
+    auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
+      const int st = i % kCtaStages;
+      const uint32_t ph = (uint32_t)(i / kCtaStages) & 1u;
+      while (!mbar_try_wait(sfull + 8 * st, ph)) {
+      }
+      const unsigned char* base = ring + st * kCtaStageBytes + sl;
+      E4 = *reinterpret_cast<const float4*>(base);
+      H4 = *reinterpret_cast<const float4*>(base + kCtaWinBytes);
+      U4 = *reinterpret_cast<const float4*>(base + 2 * kCtaWinBytes);
+      V4 = *reinterpret_cast<const float4*>(base + 3 * kCtaWinBytes);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + 8 * st);
+    };
+
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)i * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+                    En + o - 2 * pitch);
+      fetch(i + 1, E4, H4, U4, V4);
+      row_step<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
+                    En + o - pitch);
+    }
+    if (i < n) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)i * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+                    En + o - 2 * pitch);
+    }
+  }
+  if (RED >= 1) block_reduce_and_finalize<RED, kCtaStrips + 1>(acc, a.red);
 }
 
 // ---------------------------------------------------------------------------
@@ -555,7 +702,7 @@ __global__ void __launch_bounds__(kThreads) sw2d_ingest(const IngestArgs a) {
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.bad, 1);
   // reuse the fold: record[kRecSumEta] = sum(hzero)
-  block_reduce_and_finalize<1>(acc, a.red);
+  block_reduce_and_finalize<1, kWarpsPerBlock>(acc, a.red);
 }
 
 // ---------------------------------------------------------------------------
@@ -578,7 +725,7 @@ __global__ void __launch_bounds__(kThreads) sw2d_reduce_state(const ReduceArgs a
     acc.max_v = fmaxf(acc.max_v, fabsf(a.V[o]));
     acc.wet += (__fadd_rn(h0, e) < a.hmin) ? 0.0 : 1.0;
   }
-  block_reduce_and_finalize<2>(acc, a.red);
+  block_reduce_and_finalize<2, kWarpsPerBlock>(acc, a.red);
 }
 
 __global__ void sw2d_wet_mask(const float* E, const float* H0, long long pitch,
@@ -605,31 +752,59 @@ int grid_stride_blocks(long long n) {
 
 }  // namespace
 
-int step_blocks(const StepArgs& a) {
-  const long long warps = (long long)a.nstrips * a.nsegs;
-  return (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+int step_strips_per_cta(int kind) { return kind == 1 ? kCtaStrips : kStepWarps; }
+
+int step_grid(int kind, int nstrips, int nsegs) {
+  const int per = step_strips_per_cta(kind);
+  return ((nstrips + per - 1) / per) * nsegs;
 }
 
-void launch_step(const StepArgs& a, int red_level, void* stream) {
-  const int blocks = step_blocks(a);
+namespace {
+template <int RED>
+void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
+  const int blocks = step_grid(kind, a.nstrips, a.nsegs);
+  if (kind == 1) {
+    static bool attr = false;  // per process: dynamic smem above 48 KB
+    if (!attr) {
+      cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kCtaSmem);
+      attr = true;
+    }
+    sw2d_step_cta<RED><<<blocks, kCtaThreads, kCtaSmem, s>>>(a);
+  } else {
+    sw2d_step_warp<RED><<<blocks, 32 * kStepWarps, 0, s>>>(a);
+  }
+}
+
+template <int RED>
+int occupancy_kind(int kind) {
+  int n = 0;
+  if (kind == 1) {
+    cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kCtaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED>, kCtaThreads,
+                                                  kCtaSmem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_warp<RED>, 32 * kStepWarps, 0);
+  }
+  return n < 1 ? 1 : n;
+}
+}  // namespace
+
+void launch_step(const StepArgs& a, int red_level, int kind, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (red_level >= 2)
-    sw2d_step_fused<2><<<blocks, kThreads, 0, s>>>(a);
+    launch_kind<2>(a, kind, s);
   else if (red_level == 1)
-    sw2d_step_fused<1><<<blocks, kThreads, 0, s>>>(a);
+    launch_kind<1>(a, kind, s);
   else
-    sw2d_step_fused<0><<<blocks, kThreads, 0, s>>>(a);
+    launch_kind<0>(a, kind, s);
 }
 
-int step_occupancy_blocks_per_sm(int red_level) {
-  int n = 0;
-  if (red_level >= 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_fused<2>, kThreads, 0);
-  else if (red_level == 1)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_fused<1>, kThreads, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_fused<0>, kThreads, 0);
-  return n < 1 ? 1 : n;
+int step_occupancy_blocks_per_sm(int red_level, int kind) {
+  if (red_level >= 2) return occupancy_kind<2>(kind);
+  if (red_level == 1) return occupancy_kind<1>(kind);
+  return occupancy_kind<0>(kind);
 }
 
 int ingest_blocks(const IngestArgs& a) {
