@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -166,7 +167,8 @@ float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch;
 void plan_launches(sw2d* h) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  const int bps = step_occupancy_blocks_per_sm(h->red_level, h->kind);
+  int bps = step_occupancy_blocks_per_sm(h->red_level, h->kind);
+  if (const char* e = std::getenv("SW2D_CTAS_PER_SM")) bps = std::max(1, std::min(bps, std::atoi(e)));
   // one wave: resident CTAs / CTAs across the columns
   const int per = step_strips_per_cta(h->kind);
   const long long ncc = (h->nstrips + per - 1) / per;
@@ -203,6 +205,13 @@ void plan_launches(sw2d* h) {
     }
   }
   h->step_blocks = part;
+  if (std::getenv("SW2D_VERBOSE")) {
+    std::fprintf(stderr, "[sw2d] kind %d red %d: %d CTAs/SM on %d SMs, %d strips\n", h->kind,
+                 h->red_level, bps, sms, h->nstrips);
+    for (const Launch& L : h->launches)
+      std::fprintf(stderr, "[sw2d]   slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
+                   L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
+  }
 }
 
 StepArgs step_args(sw2d* h, const Launch& L, double* rec) {

@@ -554,7 +554,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 }
 
 template <int RED>
-__global__ void __launch_bounds__(kCtaThreads)
+__global__ void __launch_bounds__(kCtaThreads, 1)
     sw2d_step_cta(const StepArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
   unsigned char* ring = dsm;
@@ -563,11 +563,12 @@ __global__ void __launch_bounds__(kCtaThreads)
   const uint32_t sempty = sfull + 8 * kCtaStages;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  // the strips are spread evenly over the ncc CTA columns (7 or 8 each)
   const int ncc = (a.nstrips + kCtaStrips - 1) / kCtaStrips;
   const int cc = blockIdx.x % ncc;
   const int seg = blockIdx.x / ncc;
-  const int strip0 = cc * kCtaStrips;
-  const int nact = min(kCtaStrips, a.nstrips - strip0);   // active compute warps
+  const int strip0 = (cc * a.nstrips) / ncc;
+  const int nact = ((cc + 1) * a.nstrips) / ncc - strip0;   // active compute warps
 
   Acc acc;
   acc.init();
@@ -761,13 +762,20 @@ int step_grid(int kind, int nstrips, int nsegs) {
 
 namespace {
 template <int RED>
+void cta_attributes() {
+  cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kCtaSmem);
+  cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       100);
+}
+
+template <int RED>
 void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
   const int blocks = step_grid(kind, a.nstrips, a.nsegs);
   if (kind == 1) {
     static bool attr = false;  // per process: dynamic smem above 48 KB
     if (!attr) {
-      cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kCtaSmem);
+      cta_attributes<RED>();
       attr = true;
     }
     sw2d_step_cta<RED><<<blocks, kCtaThreads, kCtaSmem, s>>>(a);
@@ -780,8 +788,7 @@ template <int RED>
 int occupancy_kind(int kind) {
   int n = 0;
   if (kind == 1) {
-    cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kCtaSmem);
+    cta_attributes<RED>();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED>, kCtaThreads,
                                                   kCtaSmem);
   } else {
