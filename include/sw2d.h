@@ -113,6 +113,18 @@ int sw2d_abi_version(void);
 int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
                    int64_t* nrows);
 
+/* Pure host: the per-step halo exchange of rank `rank` among `nranks` row
+ * slabs (the fused step's dependency cone is 2 rows: DESIGN.md "Multi-GPU").
+ * A slab's fields are (nrows + 4)-row arrays: storage rows 0,1 are the south
+ * halo, 2 .. nrows+1 the owned rows, nrows+2, nrows+3 the north halo.  Each
+ * message is 2 consecutive storage rows of eta, u and v (of hzero once, in
+ * sw2d_set_state).  out[0] = first row sent to the south neighbour (rank-1),
+ * out[1] = first row received from it, out[2] = first row sent to the north
+ * neighbour (rank+1), out[3] = first row received from it; -1 where there is
+ * no neighbour.  Returns the number of neighbours (0..2) or SW2D_EINVAL (as
+ * sw2d_partition).  The library performs the exchange; this is its plan. */
+int sw2d_halo_plan(int64_t ny, int32_t nranks, int32_t rank, int64_t out[4]);
+
 /* Pure host: writes a fresh ncclUniqueId (128 bytes) for sw2d_dist.nccl_id.
  * SW2D_ENCCL if NCCL cannot be loaded. */
 int sw2d_nccl_unique_id(unsigned char out[128]);

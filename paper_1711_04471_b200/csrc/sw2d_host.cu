@@ -194,15 +194,14 @@ void plan_launches(sw2d* h) {
   };
   for (int s = 0; s < (int)h->slabs.size(); ++s) {
     const Slab& sl = h->slabs[s];
+    // rows within 2 of an internal slab boundary read this step's halo
+    // (phase 1, after the exchange); the rest (phase 0) overlap with it.
+    // Virtual ranks use the same bands, so one GPU exercises the split.
     const long long J0 = sl.j0 + 1, J1 = sl.j0 + sl.nrows;
-    if (h->multi) {
-      const bool lo_halo = h->rank > 0, hi_halo = h->rank < h->nranks - 1;
-      add(s, J0 + (lo_halo ? 2 : 0), J1 - (hi_halo ? 2 : 0), 0);
-      if (lo_halo) add(s, J0, J0 + 1, 1);
-      if (hi_halo) add(s, J1 - 1, J1, 1);
-    } else {
-      add(s, J0, J1, 0);
-    }
+    const bool lo_halo = sl.j0 > 0, hi_halo = sl.j0 + sl.nrows < h->p.ny;
+    add(s, J0 + (lo_halo ? 2 : 0), J1 - (hi_halo ? 2 : 0), 0);
+    if (lo_halo) add(s, J0, J0 + 1, 1);
+    if (hi_halo) add(s, J1 - 1, J1, 1);
   }
   h->step_blocks = part;
   if (std::getenv("SW2D_VERBOSE")) {
@@ -244,54 +243,64 @@ StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
   return a;
 }
 
-// Device copies of the 2-row halos between virtual-rank slabs (fields of
-// buffer `b`; hzero when b < 0).
+// Fields moved by a halo exchange: eta, u, v of buffer b (hzero when b < 0).
+int halo_fields(Slab& sl, int b, float** f) {
+  if (b < 0) {
+    f[0] = sl.H0;
+    return 1;
+  }
+  f[0] = sl.E[b];
+  f[1] = sl.U[b];
+  f[2] = sl.V[b];
+  return 3;
+}
+
+// Device copies of the 2-row halos between virtual-rank slabs, following
+// sw2d_halo_plan (the same plan the NCCL path runs).
 int virtual_halo(sw2d* h, int b) {
-  const size_t bytes = (size_t)(2 * h->pitch) * sizeof(float);
-  for (size_t s = 0; s + 1 < h->slabs.size(); ++s) {
-    Slab& lo = h->slabs[s];
-    Slab& hi = h->slabs[s + 1];
-    float* fl[3];
-    float* fh[3];
-    int nf = 3;
-    if (b < 0) {
-      fl[0] = lo.H0; fh[0] = hi.H0; nf = 1;
-    } else {
-      fl[0] = lo.E[b]; fl[1] = lo.U[b]; fl[2] = lo.V[b];
-      fh[0] = hi.E[b]; fh[1] = hi.U[b]; fh[2] = hi.V[b];
-    }
-    for (int f = 0; f < nf; ++f) {
-      CUDA_TRY(h, cudaMemcpyAsync(fld(fh[f], h->pitch, 0), fld(fl[f], h->pitch, lo.nrows),
-                                  bytes, cudaMemcpyDeviceToDevice, h->stream));
-      CUDA_TRY(h, cudaMemcpyAsync(fld(fl[f], h->pitch, lo.nrows + 2), fld(fh[f], h->pitch, 2),
-                                  bytes, cudaMemcpyDeviceToDevice, h->stream));
+  const size_t bytes = (size_t)(kHaloRows * h->pitch) * sizeof(float);
+  const int P = (int)h->slabs.size();
+  for (int r = 0; r < P; ++r) {
+    int64_t plan[4];
+    sw2d_halo_plan(h->p.ny, P, r, plan);
+    float* mine[3];
+    const int nf = halo_fields(h->slabs[r], b, mine);
+    for (int side = 0; side < 2; ++side) {  // 0: south neighbour r-1, 1: north r+1
+      const int64_t recv_row = plan[2 * side + 1];
+      if (recv_row < 0) continue;
+      const int peer = side == 0 ? r - 1 : r + 1;
+      int64_t pplan[4];
+      sw2d_halo_plan(h->p.ny, P, peer, pplan);
+      const int64_t send_row = pplan[side == 0 ? 2 : 0];  // what the peer sends towards r
+      float* theirs[3];
+      halo_fields(h->slabs[peer], b, theirs);
+      for (int f = 0; f < nf; ++f)
+        CUDA_TRY(h, cudaMemcpyAsync(fld(mine[f], h->pitch, recv_row),
+                                    fld(theirs[f], h->pitch, send_row), bytes,
+                                    cudaMemcpyDeviceToDevice, h->stream));
     }
   }
   return SW2D_OK;
 }
 
-// NCCL exchange of the 2-row halos with the row neighbours (fields of buffer
-// `b`; hzero when b < 0), enqueued on stream `st`.
+// NCCL exchange of the 2-row halos with the row neighbours following
+// sw2d_halo_plan, enqueued on stream `st`.
 int nccl_halo(sw2d* h, int b, cudaStream_t st) {
   const auto& nc = sw2d_host::nccl();
-  Slab& sl = h->slabs[0];
+  int64_t plan[4];
+  sw2d_halo_plan(h->p.ny, h->nranks, h->rank, plan);
   float* f[3];
-  int nf = 3;
-  if (b < 0) {
-    f[0] = sl.H0; nf = 1;
-  } else {
-    f[0] = sl.E[b]; f[1] = sl.U[b]; f[2] = sl.V[b];
-  }
-  const size_t cnt = (size_t)(2 * h->pitch);
+  const int nf = halo_fields(h->slabs[0], b, f);
+  const size_t cnt = (size_t)(kHaloRows * h->pitch);
   NCCL_TRY(h, nc.GroupStart());
   for (int i = 0; i < nf; ++i) {
-    if (h->rank > 0) {  // south neighbour
-      NCCL_TRY(h, nc.Send(fld(f[i], h->pitch, 2), cnt, ncclFloat32, h->rank - 1, h->comm_nccl, st));
-      NCCL_TRY(h, nc.Recv(fld(f[i], h->pitch, 0), cnt, ncclFloat32, h->rank - 1, h->comm_nccl, st));
-    }
-    if (h->rank < h->nranks - 1) {  // north neighbour
-      NCCL_TRY(h, nc.Send(fld(f[i], h->pitch, sl.nrows), cnt, ncclFloat32, h->rank + 1, h->comm_nccl, st));
-      NCCL_TRY(h, nc.Recv(fld(f[i], h->pitch, sl.nrows + 2), cnt, ncclFloat32, h->rank + 1, h->comm_nccl, st));
+    for (int side = 0; side < 2; ++side) {
+      if (plan[2 * side] < 0) continue;
+      const int peer = side == 0 ? h->rank - 1 : h->rank + 1;
+      NCCL_TRY(h, nc.Send(fld(f[i], h->pitch, plan[2 * side]), cnt, ncclFloat32, peer,
+                          h->comm_nccl, st));
+      NCCL_TRY(h, nc.Recv(fld(f[i], h->pitch, plan[2 * side + 1]), cnt, ncclFloat32, peer,
+                          h->comm_nccl, st));
     }
   }
   NCCL_TRY(h, nc.GroupEnd());
@@ -452,6 +461,20 @@ int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
   *j0 = (int64_t)rank * base + std::min<int64_t>(rank, rem);
   *nrows = n;
   return SW2D_OK;
+}
+
+int sw2d_halo_plan(int64_t ny, int32_t nranks, int32_t rank, int64_t out[4]) {
+  int64_t j0, nrows;
+  if (!out) return SW2D_EINVAL;
+  const int rc = sw2d_partition(ny, nranks, rank, &j0, &nrows);
+  if (rc != SW2D_OK) return rc;
+  // storage rows: 0,1 south halo | 2 .. nrows+1 owned | nrows+2, nrows+3 north halo
+  const bool south = rank > 0, north = rank < nranks - 1;
+  out[0] = south ? kHaloRows : -1;           // first owned rows -> south neighbour
+  out[1] = south ? 0 : -1;                   // its last owned rows -> south halo
+  out[2] = north ? nrows : -1;               // last owned rows -> north neighbour
+  out[3] = north ? nrows + kHaloRows : -1;   // its first owned rows -> north halo
+  return (south ? 1 : 0) + (north ? 1 : 0);
 }
 
 int sw2d_nccl_unique_id(unsigned char out[128]) {

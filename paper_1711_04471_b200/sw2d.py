@@ -26,7 +26,7 @@ SW2D_RED_N = 7
 SW2D_VARIANT_FUSED = 0
 
 #: every symbol include/sw2d.h declares (checked by tests/test_abi.py)
-SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_nccl_unique_id",
+SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",
            "sw2d_create", "sw2d_local_rows", "sw2d_set_state", "sw2d_step",
            "sw2d_reduce", "sw2d_reduce_history", "sw2d_get_state", "sw2d_sync",
            "sw2d_launch_count", "sw2d_destroy", "sw2d_strerror",
@@ -71,6 +71,7 @@ def load(path: str = _LIB_PATH):
     sig = {
         "sw2d_abi_version": ([], ctypes.c_int),
         "sw2d_partition": ([i64, i32, i32, p64, p64], ctypes.c_int),
+        "sw2d_halo_plan": ([i64, i32, i32, p64], ctypes.c_int),
         "sw2d_nccl_unique_id": ([vp], ctypes.c_int),
         "sw2d_create": ([ctypes.POINTER(sw2d_params), ctypes.POINTER(sw2d_dist), vp,
                          ctypes.POINTER(vp)], ctypes.c_int),
@@ -144,6 +145,16 @@ def sw2d_partition(ny: int, nranks: int, rank: int):
     _check(load().sw2d_partition(int(ny), int(nranks), int(rank),
                                  ctypes.byref(j0), ctypes.byref(n)))
     return j0.value, n.value
+
+
+def sw2d_halo_plan(ny: int, nranks: int, rank: int):
+    """(send_south, recv_south, send_north, recv_north) first storage rows of
+    the 2-row halo messages of `rank` (-1: no neighbour)."""
+    out = (ctypes.c_int64 * 4)()
+    rc = load().sw2d_halo_plan(int(ny), int(nranks), int(rank), out)
+    if rc < 0:
+        _check(rc)
+    return tuple(int(x) for x in out)
 
 
 def sw2d_nccl_unique_id() -> bytes:
