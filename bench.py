@@ -41,6 +41,7 @@ import sw2d_inputs as si  # noqa: E402
 METRIC = "2DSW cell-updates/s at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "cell-updates/s"
 BYTES_PER_CELL = 28          # fused step: read eta,u,v,hzero (16 B) + write eta,u,v (12 B)
+PAPER_BYTES_PER_CELL = 75   # paper-shaped variant: 21 + 20 + 34 B over its 3 map kernels
 FALLBACK_HBM_GBS = 6650.0    # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
 
 
@@ -55,6 +56,8 @@ def parse():
                     help="model time steps per bench step (default 100; c2: 10000)")
     ap.add_argument("--reduce", choices=["default", "none", "volume", "all"], default="default",
                     help="per-step fused diagnostics (default: VOLUME for c5, none otherwise)")
+    ap.add_argument("--variant", choices=["fused", "paper"], default="fused",
+                    help="paper: the paper-shaped 3-map-kernel step (NEXT-1, comparison)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -242,7 +245,9 @@ def run_ours(args, cfg, ws, rank, local):
     stream = torch.cuda.Stream()          # the handle's stream; events are recorded on it
     torch.cuda.set_stream(stream)
     p = sw2d.make_params(nx, ny, cfg["dx"], cfg["dy"], cfg["dt"], cfg["g"], cfg["eps"],
-                         cfg["hmin"], reduce_every_step=mask, history_len=max(T, 1))
+                         cfg["hmin"], reduce_every_step=mask, history_len=max(T, 1),
+                         variant=sw2d.SW2D_VARIANT_PAPER if args.variant == "paper"
+                         else sw2d.SW2D_VARIANT_FUSED)
     h = sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid), stream)
 
     def barrier():
@@ -284,12 +289,15 @@ def run_ours(args, cfg, ws, rank, local):
         step_launches_per_model_step = launches / (T * args.steps)
         t_step_s = ms * 1e-3 / (T * args.steps)
         cells_local = nrows * nx
-        achieved = BYTES_PER_CELL * cells_local / t_step_s / 1e9
+        bpc = BYTES_PER_CELL if args.variant == "fused" else PAPER_BYTES_PER_CELL
+        achieved = bpc * cells_local / t_step_s / 1e9
         peak, peak_src = hbm_peak()
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]),
-                "algorithmic_bytes_per_launch": BYTES_PER_CELL * cells_local,
-                "kernel": "sw2d_step_fused<%d>" % (0 if not mask else (1 if mask < 4 else 2)),
+                "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]) if args.variant == "fused" else None,
+                "algorithmic_bytes_per_launch": bpc * cells_local,
+                "kernel": ("sw2d_step_cta<%d>" % (0 if not mask else (1 if mask < 4 else 2)))
+                if args.variant == "fused" else
+                "paper_momentum + paper_continuity + paper_shapiro_update (per step)",
                 "launches_per_model_step": step_launches_per_model_step,
                 "peak_source": peak_src,
                 "note": "per-model-step time of the whole timed region (the step kernel "

@@ -77,7 +77,10 @@ enum {
 
 /* Step-kernel variants (sw2d_params.variant). */
 enum {
-  SW2D_VARIANT_FUSED = 0 /* one fused pass per step: 28 B/cell-step */
+  SW2D_VARIANT_FUSED = 0, /* one fused pass per step: 28 B/cell-step   */
+  SW2D_VARIANT_PAPER = 1  /* the paper's shape: three map kernels per step, h and
+                             wet stored: 75 B/cell-step; one GPU,
+                             no virtual or real ranks; for comparison            */
 };
 
 typedef struct {

@@ -31,6 +31,8 @@ constexpr int kDefaultHistory = 1024;
 
 struct Slab {
   int64_t j0 = 0, nrows = 0;  // 0-based global first owned row, owned rows
+  float* Hs = nullptr;                     // paper variant: stored depth h
+  unsigned char* W[2] = {nullptr, nullptr};  // paper variant: wet flags
   float* H0 = nullptr;
   float* E[2] = {nullptr, nullptr};
   float* U[2] = {nullptr, nullptr};
@@ -77,6 +79,7 @@ struct sw2d {
   unsigned char* wetbuf = nullptr;
   size_t wetbuf_bytes = 0;
   int64_t steps = 0;
+  int wcur = 0;  // paper variant: current wet buffer
   bool state_set = false;
   bool pending_allreduce = false;
   int64_t pending_step = 0;
@@ -128,7 +131,9 @@ bool finite_pos(float x) { return std::isfinite(x) && x > 0.0f; }
 int validate(const sw2d_params* p, std::string& why) {
   if (!p) { why = "params is NULL"; return SW2D_EINVAL; }
   if (p->bc != SW2D_BC_CLOSED) { why = "bc must be SW2D_BC_CLOSED"; return SW2D_EUNSUPPORTED; }
-  if (p->variant != SW2D_VARIANT_FUSED) { why = "unknown variant"; return SW2D_EUNSUPPORTED; }
+  if (p->variant != SW2D_VARIANT_FUSED && p->variant != SW2D_VARIANT_PAPER) {
+    why = "unknown variant"; return SW2D_EUNSUPPORTED;
+  }
   if (p->nx < 1 || p->ny < 1) { why = "nx, ny must be >= 1"; return SW2D_EINVAL; }
   if (p->nx > (1LL << 30)) { why = "nx too large"; return SW2D_EINVAL; }
   if (!finite_pos(p->dx) || !finite_pos(p->dy) || !finite_pos(p->dt)) {
@@ -243,6 +248,62 @@ StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
   return a;
 }
 
+PaperArgs paper_args(sw2d* h, Slab& sl) {
+  PaperArgs a;
+  a.E = sl.E[0];
+  a.U = sl.U[0];
+  a.V = sl.V[0];
+  a.H0 = sl.H0;
+  a.un = sl.U[1];
+  a.vn = sl.V[1];
+  a.etan = sl.E[1];
+  a.h = sl.Hs;
+  a.wet_in = sl.W[h->wcur];
+  a.wet_out = sl.W[1 - h->wcur];
+  a.Eo = sl.E[0];
+  a.Uo = sl.U[0];
+  a.Vo = sl.V[0];
+  a.pitch = h->pitch;
+  a.jbase = sl.j0 + 1 - kHaloRows;
+  a.nrows = sl.nrows;
+  a.nx = (int)h->p.nx;
+  a.ny = h->p.ny;
+  a.c = h->coef;
+  return a;
+}
+
+// Diagnostics of the current state into `rec` with the standalone kernel.
+int reduce_into(sw2d* h, double* rec) {
+  int expected = 0;
+  std::vector<ReduceArgs> ras;
+  for (Slab& s : h->slabs) {
+    ReduceArgs a{};
+    a.E = s.E[h->cur];
+    a.U = s.U[h->cur];
+    a.V = s.V[h->cur];
+    a.H0 = s.H0;
+    a.pitch = h->pitch;
+    a.nrows = s.nrows;
+    a.nx = (int)h->p.nx;
+    a.hmin = h->p.hmin;
+    a.red.part_base = expected;
+    expected += reduce_blocks(a);
+    ras.push_back(a);
+  }
+  for (ReduceArgs& a : ras) {
+    a.red.partials = h->partials;
+    a.red.counter = h->counter;
+    a.red.expected = expected;
+    a.red.rec = rec;
+    a.red.h0sum = h->h0sum;
+    a.red.dxdy = (double)h->p.dx * (double)h->p.dy;
+    launch_reduce(a, h->stream);
+    h->nlaunch++;
+  }
+  CUDA_TRY(h, cudaGetLastError());
+  return SW2D_OK;
+}
+
 // Fields moved by a halo exchange: eta, u, v of buffer b (hzero when b < 0).
 int halo_fields(Slab& sl, int b, float** f) {
   if (b < 0) {
@@ -331,6 +392,9 @@ double rec_value(const double* rec, int op) {
 
 void free_all(sw2d* h) {
   for (Slab& s : h->slabs) {
+    cudaFree(s.Hs);
+    cudaFree(s.W[0]);
+    cudaFree(s.W[1]);
     cudaFree(s.H0);
     for (int b = 0; b < 2; ++b) {
       cudaFree(s.E[b]);
@@ -372,6 +436,8 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     if (dist->device >= 0) CUDA_TRY(h, cudaSetDevice(dist->device));
   }
   CUDA_TRY(h, cudaGetDevice(&h->device));
+  if (h->p.variant == SW2D_VARIANT_PAPER && h->nranks > 1)
+    return fail(h, SW2D_EUNSUPPORTED, "the paper variant runs on one GPU without ranks");
   // slabs
   if (h->virt) {
     for (int r = 0; r < h->nranks; ++r) {
@@ -406,6 +472,15 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     for (float** f : all) {
       CUDA_TRY(h, cudaMalloc(f, bytes));
       CUDA_TRY(h, cudaMemsetAsync(*f, 0, bytes, h->stream));
+    }
+    if (h->p.variant == SW2D_VARIANT_PAPER) {
+      const size_t wbytes = (size_t)(s.nrows + 2 * kHaloRows) * (size_t)h->pitch;
+      CUDA_TRY(h, cudaMalloc(&s.Hs, bytes));
+      CUDA_TRY(h, cudaMemsetAsync(s.Hs, 0, bytes, h->stream));
+      for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(h, cudaMalloc(&s.W[b], wbytes));
+        CUDA_TRY(h, cudaMemsetAsync(s.W[b], 0, wbytes, h->stream));
+      }
     }
   }
   plan_launches(h);
@@ -582,6 +657,16 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
     int rc = nccl_halo(h, -1, h->stream);
     if (rc) return rc;
   }
+  h->wcur = 0;
+  if (h->p.variant == SW2D_VARIANT_PAPER) {
+    for (Slab& s : h->slabs) {
+      PaperArgs a = paper_args(h, s);
+      a.wet_out = s.W[0];
+      launch_paper_init(a, h->stream);
+      h->nlaunch++;
+    }
+    CUDA_TRY(h, cudaGetLastError());
+  }
   int bad = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -599,6 +684,22 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
   ENTER(h);
   if (nsteps < 0) return fail(h, SW2D_EINVAL, "nsteps must be >= 0");
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_step before sw2d_set_state");
+  if (h->p.variant == SW2D_VARIANT_PAPER) {
+    for (int64_t i = 0; i < nsteps; ++i) {
+      for (Slab& s : h->slabs) {
+        launch_paper_step(paper_args(h, s), h->stream);
+        h->nlaunch += 3;
+      }
+      CUDA_TRY(h, cudaGetLastError());
+      h->wcur = 1 - h->wcur;
+      if (h->red_level) {
+        int rc = reduce_into(h, h->hist + (size_t)(h->steps % h->hist_len) * kRecN);
+        if (rc) return rc;
+      }
+      h->steps++;
+    }
+    return SW2D_OK;
+  }
   for (int64_t i = 0; i < nsteps; ++i) {
     double* rec = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
     if (h->virt) {
@@ -669,33 +770,10 @@ int sw2d_reduce(sw2d* h, int op, double* out) {
   ENTER(h);
   if (!out || op < 0 || op >= SW2D_RED_N) return fail(h, SW2D_EINVAL, "bad op / out");
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_reduce before sw2d_set_state");
-  int expected = 0;
-  std::vector<ReduceArgs> ras;
-  for (Slab& s : h->slabs) {
-    ReduceArgs a{};
-    a.E = s.E[h->cur];
-    a.U = s.U[h->cur];
-    a.V = s.V[h->cur];
-    a.H0 = s.H0;
-    a.pitch = h->pitch;
-    a.nrows = s.nrows;
-    a.nx = (int)h->p.nx;
-    a.hmin = h->p.hmin;
-    a.red.part_base = expected;
-    expected += reduce_blocks(a);
-    ras.push_back(a);
+  {
+    int rc = reduce_into(h, h->rec);
+    if (rc) return rc;
   }
-  for (ReduceArgs& a : ras) {
-    a.red.partials = h->partials;
-    a.red.counter = h->counter;
-    a.red.expected = expected;
-    a.red.rec = h->rec;
-    a.red.h0sum = h->h0sum;
-    a.red.dxdy = (double)h->p.dx * (double)h->p.dy;
-    launch_reduce(a, h->stream);
-    h->nlaunch++;
-  }
-  CUDA_TRY(h, cudaGetLastError());
   if (h->multi) {
     int rc = nccl_allreduce_rec(h, h->rec, h->stream);
     if (rc) return rc;

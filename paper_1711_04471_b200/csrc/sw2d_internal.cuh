@@ -121,6 +121,32 @@ struct ReduceArgs {
 int reduce_blocks(const ReduceArgs& a);
 void launch_reduce(const ReduceArgs& a, void* stream);
 
+// The paper-shaped unfused step (sw2d_paper_kernels.cu): three map kernels
+// per step, h and wet stored (SW2D_VARIANT_PAPER).
+struct PaperArgs {
+  const float* E;            // state n: eta, u, v (read by K1/K2)
+  const float* U;
+  const float* V;
+  const float* H0;
+  float* un;                 // scratch: K1 -> K2, K3
+  float* vn;
+  float* etan;               // scratch: K2 -> K3
+  float* h;                  // stored depth (K3 writes, K2 reads next step)
+  const unsigned char* wet_in;   // start-of-step wet flags
+  unsigned char* wet_out;        // end-of-step wet flags
+  float* Eo;                 // state n+1 (in place: K3 writes E, U, V)
+  float* Uo;
+  float* Vo;
+  long long pitch;           // elements per storage row (floats and flags)
+  long long jbase;
+  long long nrows;
+  int nx;
+  long long ny;
+  Coef c;
+};
+void launch_paper_step(const PaperArgs& a, void* stream);   // 3 launches
+void launch_paper_init(const PaperArgs& a, void* stream);   // h, wet_out from H0 + E
+
 // wet mask of the current state into a dense uint8 [nrows][nx] buffer.
 void launch_wet(const float* E, const float* H0, long long pitch,
                 long long nrows, int nx, float hmin, unsigned char* out,

@@ -35,10 +35,6 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__device__ __forceinline__ float4 ldg4(const float* p) {
-  return __ldg(reinterpret_cast<const float4*>(p));
-}
-
 __device__ __forceinline__ void st4(float* p, float a, float b, float c,
                                     float d) {
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);

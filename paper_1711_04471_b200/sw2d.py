@@ -24,6 +24,7 @@ SW2D_BC_CLOSED = 0
  SW2D_RED_MAX_ABS_U, SW2D_RED_MAX_ABS_V, SW2D_RED_WET_COUNT) = range(7)
 SW2D_RED_N = 7
 SW2D_VARIANT_FUSED = 0
+SW2D_VARIANT_PAPER = 1
 
 #: every symbol include/sw2d.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",

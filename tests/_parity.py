@@ -46,14 +46,15 @@ def oracle_run(params, state, nsteps, history=False):
     return (out[0], out[1], out[2], w) + ((out[3],) if history else ())
 
 
-def gpu_run(params, state, nsteps, reduce_mask=0, dist=None, chunks=None):
+def gpu_run(params, state, nsteps, reduce_mask=0, dist=None, chunks=None,
+            variant=sw2d.SW2D_VARIANT_FUSED):
     """Create a handle, upload, step (optionally in chunks), download."""
     hz, e, u, v = state
     ny, nx = hz.shape
     p = sw2d.make_params(nx, ny, params["dx"], params["dy"], params["dt"],
                          params["g"], params["eps"], params["hmin"],
                          reduce_every_step=reduce_mask,
-                         history_len=max(nsteps, 1))
+                         history_len=max(nsteps, 1), variant=variant)
     h = sw2d.sw2d_create(p, dist)
     try:
         sw2d.sw2d_set_state(h, hz, e, u, v)

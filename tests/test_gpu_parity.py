@@ -293,3 +293,43 @@ def test_c5_bench_configuration_sampled_parity():
     _window_parity(cfg, got, n, _sample_centers(cfg, got), size=32)
     assert np.max(np.abs(hist - v0)) <= 1e-6 * v0
     assert abs(hist[-1] - red[sw2d.SW2D_RED_VOLUME]) <= 1e-9 * v0
+
+
+# --- the paper-shaped unfused variant (NEXT-1): same parity bar ------------
+
+@pytest.mark.parametrize("nx,ny,n", [(100, 100, 100), (517, 389, 100), (1, 9, 25), (9, 1, 25),
+                                     (3, 3, 1)])
+def test_paper_variant_bitwise(nx, ny, n):
+    if (nx, ny) == (100, 100):
+        st = si.generate(si.config("c1"))
+    else:
+        st = _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny)
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, launches = gpu_run(P, st, n, reduce_mask=ALL,
+                                       variant=sw2d.SW2D_VARIANT_PAPER)
+    assert_state_equal(got, want[:4], where=f"paper variant {nx}x{ny}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    for op, series in hist.items():
+        for k in range(n):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[k]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want[4][k, op]
+            check_reductions(row, ref)
+    assert launches >= 3 * n
+
+
+def test_paper_variant_rejects_ranks():
+    with pytest.raises(sw2d.Sw2dError) as ei:
+        sw2d.sw2d_create(sw2d.make_params(64, 64, variant=sw2d.SW2D_VARIANT_PAPER),
+                         sw2d.make_dist(0, 2, virtual_ranks=1))
+    assert ei.value.code == sw2d.SW2D_EUNSUPPORTED
+
+
+def _random_state(nx, ny):
+    rng = np.random.default_rng(nx * 7919 + ny)
+    hz = rng.uniform(-1.0, 3.0, (ny, nx)).astype(np.float32)
+    e = np.where(hz < 0, -hz, rng.uniform(-0.2, 0.4, (ny, nx))).astype(np.float32)
+    u = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
+    v = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
+    return hz, e, u, v
