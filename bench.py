@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4"], default="c5")
+    ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4", "p1000", "p2000"], default="c5")
     ap.add_argument("--substeps", type=int, default=None,
                     help="model time steps per bench step (default 100; c2: 10000)")
     ap.add_argument("--reduce", choices=["default", "none", "volume", "all"], default="default",
@@ -145,7 +145,7 @@ def dist_env():
 
 
 def default_substeps(workload):
-    return 10000 if workload == "c2" else 100
+    return 10000 if workload in ("c2", "p1000", "p2000") else 100
 
 
 # ---------------------------------------------------------------------------

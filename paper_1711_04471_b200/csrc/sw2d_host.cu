@@ -26,7 +26,7 @@ namespace {
 
 thread_local std::string t_create_err;
 
-constexpr int kMinRowsPerSeg = 8;
+constexpr int kMinRowsPerSeg = 4;   // small grids: more, shorter segments (latency-bound)
 constexpr int kDefaultHistory = 1024;
 
 struct Slab {
@@ -178,13 +178,15 @@ void plan_launches(sw2d* h) {
   const int per = step_strips_per_cta(h->kind);
   const long long ncc = (h->nstrips + per - 1) / per;
   const long long target_segs = std::max(1LL, (long long)sms * bps / ncc);
+  long long min_rows = kMinRowsPerSeg;
+  if (const char* e = std::getenv("SW2D_MIN_ROWS")) min_rows = std::max(1, std::atoi(e));
   h->launches.clear();
   int part = 0;
   auto add = [&](int s, long long lo, long long hi, int phase) {
     if (hi < lo) return;
     const long long rows = hi - lo + 1;
     long long rps = (rows + target_segs - 1) / target_segs;
-    rps = std::max<long long>(rps, kMinRowsPerSeg);
+    rps = std::max<long long>(rps, min_rows);
     Launch L;
     L.slab = s;
     L.row_lo = lo;

@@ -55,6 +55,11 @@ CONFIGS = {
                seed=1711044715, steps=1000, per_gpu_rows=16384,
                desc="2DSW weak scaling: 16384x16384 per GPU at 1/2/4/8 B200 "
                     "with per-step global-volume reduction"),
+    # the paper's other 2DSW sizes, for the small-grid study
+    "p1000": dict(nx=1000, ny=1000, kind="flat", amp=0.5, sigma=50.0, seed=0, steps=10000,
+                  desc="2DSW 1000x1000 (paper size), flat basin, 10k steps"),
+    "p2000": dict(nx=2000, ny=2000, kind="flat", amp=0.5, sigma=100.0, seed=0, steps=10000,
+                  desc="2DSW 2000x2000 (paper size), flat basin, 10k steps"),
 }
 
 _M64 = (1 << 64) - 1
