@@ -58,6 +58,8 @@ def parse():
                     help="per-step fused diagnostics (default: VOLUME for c5, none otherwise)")
     ap.add_argument("--variant", choices=["fused", "paper"], default="fused",
                     help="paper: the paper-shaped 3-map-kernel step (NEXT-1, comparison)")
+    ap.add_argument("--halo", choices=["nccl", "p2p"], default="nccl",
+                    help="N>1 halo exchange: NCCL send/recv, or fused P2P stores (IPC)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -248,7 +250,8 @@ def run_ours(args, cfg, ws, rank, local):
                          cfg["hmin"], reduce_every_step=mask, history_len=max(T, 1),
                          variant=sw2d.SW2D_VARIANT_PAPER if args.variant == "paper"
                          else sw2d.SW2D_VARIANT_FUSED)
-    h = sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid), stream)
+    halo = sw2d.SW2D_HALO_P2P if args.halo == "p2p" else sw2d.SW2D_HALO_NCCL
+    h = sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid, halo), stream)
 
     def barrier():
         if ws > 1:

@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define SW2D_ABI_VERSION 1
+#define SW2D_ABI_VERSION 2
 
 typedef struct sw2d sw2d; /* opaque, library-owned */
 
@@ -97,12 +97,23 @@ typedef struct {
                           default 1024                                            */
 } sw2d_params;
 
+/* Halo exchange between row slabs (sw2d_dist.halo_mode). */
+enum {
+  SW2D_HALO_NCCL = 0, /* grouped ncclSend/ncclRecv of the 2 boundary rows on a comm
+                         stream, overlapped with the interior launch (default)    */
+  SW2D_HALO_P2P = 1   /* fused: the boundary launch of each step stores its rows
+                         straight into the neighbours' halo rows (peer memory over
+                         NVLink via CUDA IPC; another slab's buffers for virtual
+                         ranks) and signals them with stream memory operations   */
+};
+
 typedef struct {
   int32_t rank, nranks;  /* row slabs along y (balanced); nrows >= 4 per rank     */
   int32_t device;        /* CUDA ordinal for this rank (-1: current device)       */
   int32_t virtual_ranks; /* 1: run all nranks slabs in this one handle on one
                             device, halos copied device-to-device (no NCCL); the
                             handle then owns the whole grid (test mode)          */
+  int32_t halo_mode;     /* SW2D_HALO_*                                           */
   unsigned char nccl_id[128]; /* ncclUniqueId from rank 0 (sw2d_nccl_unique_id),
                                  broadcast by the caller (e.g. torch.distributed) */
 } sw2d_dist;

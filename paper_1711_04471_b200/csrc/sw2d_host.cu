@@ -87,6 +87,17 @@ struct sw2d {
   std::string err;
   ncclComm_t comm_nccl = nullptr;
   int64_t nlaunch = 0;
+  // P2P halo mode
+  int halo_mode = SW2D_HALO_NCCL;
+  unsigned int* flags = nullptr;  // [0]: written by the south neighbour, [1]: by the north
+  struct Peer {
+    bool present = false;
+    float* E[2] = {nullptr, nullptr};
+    float* U[2] = {nullptr, nullptr};
+    float* V[2] = {nullptr, nullptr};
+    unsigned int* flags = nullptr;
+    long long jbase = 0;
+  } nbr[2];                       // [0]: south (rank-1), [1]: north (rank+1); IPC-mapped
 };
 
 namespace {
@@ -248,6 +259,41 @@ StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
   a.red.h0sum = h->h0sum;
   a.red.dxdy = (double)h->p.dx * (double)h->p.dy;
   return a;
+}
+
+// P2P halo mode: the rows of slab L.slab that its neighbours need (its first
+// two rows go south, its last two north) are mirrored into their buffers of
+// the next state.
+void set_remotes(sw2d* h, const Launch& L, StepArgs& a) {
+  for (int side = 0; side < 2; ++side) {
+    a.rem[side].lo = 1;
+    a.rem[side].hi = 0;  // none
+  }
+  const Slab& sl = h->slabs[L.slab];
+  const long long J0 = sl.j0 + 1, J1 = sl.j0 + sl.nrows;
+  const int nb = 1 - h->cur;  // the buffer being written this step
+  for (int side = 0; side < 2; ++side) {
+    float *E = nullptr, *U = nullptr, *V = nullptr;
+    long long jb = 0;
+    if (h->virt) {
+      const int peer = L.slab + (side == 0 ? -1 : 1);
+      if (peer < 0 || peer >= (int)h->slabs.size()) continue;
+      const Slab& ps = h->slabs[peer];
+      E = ps.E[nb]; U = ps.U[nb]; V = ps.V[nb];
+      jb = ps.j0 + 1 - kHaloRows;
+    } else {
+      const auto& pr = h->nbr[side];
+      if (!pr.present) continue;
+      E = pr.E[nb]; U = pr.U[nb]; V = pr.V[nb];
+      jb = pr.jbase;
+    }
+    a.rem[side].En = E;
+    a.rem[side].Un = U;
+    a.rem[side].Vn = V;
+    a.rem[side].jbase = jb;
+    a.rem[side].lo = (int)(side == 0 ? J0 : J1 - 1);
+    a.rem[side].hi = (int)(side == 0 ? J0 + 1 : J1);
+  }
 }
 
 PaperArgs paper_args(sw2d* h, Slab& sl) {
@@ -417,7 +463,64 @@ void free_all(sw2d* h) {
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);
   if (h->comm) cudaStreamDestroy(h->comm);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  for (auto& pr : h->nbr) {
+    if (!pr.present) continue;
+    for (int b = 0; b < 2; ++b) {
+      if (pr.E[b]) cudaIpcCloseMemHandle(pr.E[b]);
+      if (pr.U[b]) cudaIpcCloseMemHandle(pr.U[b]);
+      if (pr.V[b]) cudaIpcCloseMemHandle(pr.V[b]);
+    }
+    if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
+  }
+  cudaFree(h->flags);
   if (h->comm_nccl && sw2d_host::nccl().ok) sw2d_host::nccl().CommDestroy(h->comm_nccl);
+}
+
+// P2P halo mode across real ranks: export this rank's six state buffers and
+// its flag words with CUDA IPC, all-gather the handles over NCCL, and map the
+// row neighbours' buffers (NVLink peer memory).
+int setup_p2p(sw2d* h) {
+  const auto& nc = sw2d_host::nccl();
+  if (!sw2d_host::memops().ok)
+    return fail(h, SW2D_EUNSUPPORTED, "cuStreamWaitValue32/WriteValue32 unavailable");
+  CUDA_TRY(h, cudaMalloc(&h->flags, 2 * sizeof(unsigned int)));
+  CUDA_TRY(h, cudaMemset(h->flags, 0, 2 * sizeof(unsigned int)));
+  constexpr int kH = 7;
+  Slab& sl = h->slabs[0];
+  void* mine[kH] = {sl.E[0], sl.E[1], sl.U[0], sl.U[1], sl.V[0], sl.V[1], h->flags};
+  std::vector<cudaIpcMemHandle_t> hs(kH);
+  for (int i = 0; i < kH; ++i) CUDA_TRY(h, cudaIpcGetMemHandle(&hs[i], mine[i]));
+  const size_t per = kH * sizeof(cudaIpcMemHandle_t);
+  unsigned char* dsend = nullptr;
+  unsigned char* drecv = nullptr;
+  CUDA_TRY(h, cudaMalloc(&dsend, per));
+  CUDA_TRY(h, cudaMalloc(&drecv, per * (size_t)h->nranks));
+  std::vector<unsigned char> all(per * (size_t)h->nranks);
+  CUDA_TRY(h, cudaMemcpy(dsend, hs.data(), per, cudaMemcpyHostToDevice));
+  NCCL_TRY(h, nc.AllGather(dsend, drecv, per, ncclUint8, h->comm_nccl, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  CUDA_TRY(h, cudaMemcpy(all.data(), drecv, all.size(), cudaMemcpyDeviceToHost));
+  cudaFree(dsend);
+  cudaFree(drecv);
+  for (int side = 0; side < 2; ++side) {
+    const int peer = side == 0 ? h->rank - 1 : h->rank + 1;
+    if (peer < 0 || peer >= h->nranks) continue;
+    auto& pr = h->nbr[side];
+    const cudaIpcMemHandle_t* ph =
+        reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + per * (size_t)peer);
+    void* p[kH];
+    for (int i = 0; i < kH; ++i)
+      CUDA_TRY(h, cudaIpcOpenMemHandle(&p[i], ph[i], cudaIpcMemLazyEnablePeerAccess));
+    pr.E[0] = (float*)p[0]; pr.E[1] = (float*)p[1];
+    pr.U[0] = (float*)p[2]; pr.U[1] = (float*)p[3];
+    pr.V[0] = (float*)p[4]; pr.V[1] = (float*)p[5];
+    pr.flags = (unsigned int*)p[6];
+    int64_t j0, nrows;
+    sw2d_partition(h->p.ny, h->nranks, peer, &j0, &nrows);
+    pr.jbase = j0 + 1 - kHaloRows;
+    pr.present = true;
+  }
+  return SW2D_OK;
 }
 
 int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
@@ -435,6 +538,10 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     h->nranks = dist->nranks;
     h->virt = dist->virtual_ranks != 0;
     h->multi = !h->virt && h->nranks > 1;
+    if (dist->halo_mode != SW2D_HALO_NCCL && dist->halo_mode != SW2D_HALO_P2P)
+      return fail(h, SW2D_EINVAL, "unknown halo_mode");
+    h->halo_mode = dist->halo_mode;
+    if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
     if (dist->device >= 0) CUDA_TRY(h, cudaSetDevice(dist->device));
   }
   CUDA_TRY(h, cudaGetDevice(&h->device));
@@ -517,6 +624,10 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     ncclUniqueId id;
     std::memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
     NCCL_TRY(h, nc.CommInitRank(&h->comm_nccl, h->nranks, id, h->rank));
+    if (h->halo_mode == SW2D_HALO_P2P) {
+      int rc = setup_p2p(h);
+      if (rc) return rc;
+    }
   }
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return SW2D_OK;
@@ -651,13 +762,19 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
   CUDA_TRY(h, cudaGetLastError());
   CUDA_TRY(h, cudaMemcpyAsync(h->h0sum, h->rec + kRecSumEta, sizeof(double),
                               cudaMemcpyDeviceToDevice, h->stream));
-  // static hzero halo, once
+  // static hzero halo, once; in P2P mode also the state-0 halos (later steps
+  // deliver them with the boundary rows).  The flags are reset before the
+  // exchange: a neighbour can signal only after it has exchanged with us.
+  const bool p2p = h->halo_mode == SW2D_HALO_P2P;
+  if (h->flags) CUDA_TRY(h, cudaMemsetAsync(h->flags, 0, 2 * sizeof(unsigned int), h->stream));
   if (h->virt) {
     int rc = virtual_halo(h, -1);
     if (rc) return rc;
+    if (p2p && (rc = virtual_halo(h, 0))) return rc;
   } else if (h->multi) {
     int rc = nccl_halo(h, -1, h->stream);
     if (rc) return rc;
+    if (p2p && (rc = nccl_halo(h, 0, h->stream))) return rc;
   }
   h->wcur = 0;
   if (h->p.variant == SW2D_VARIANT_PAPER) {
@@ -702,13 +819,15 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
     }
     return SW2D_OK;
   }
+  const bool p2p = h->halo_mode == SW2D_HALO_P2P && (h->virt || h->multi);
+  const auto& mo = sw2d_host::memops();
   for (int64_t i = 0; i < nsteps; ++i) {
     double* rec = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
-    if (h->virt) {
+    if (h->virt && !p2p) {
       int rc = virtual_halo(h, h->cur);
       if (rc) return rc;
     }
-    if (h->multi) {
+    if (h->multi && !p2p) {
       CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
       int rc = nccl_halo(h, h->cur, h->comm);
       if (rc) return rc;
@@ -720,24 +839,53 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
         h->pending_allreduce = false;
       }
     }
-    for (int phase = 0; phase < 2; ++phase) {
-      bool waited = false;
-      for (const Launch& L : h->launches) {
-        if (L.phase != phase) continue;
-        if (phase == 1 && !waited) {
-          CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-          waited = true;
-        }
+    // phase 0: rows that read no halo of this step (overlaps the exchange)
+    for (const Launch& L : h->launches)
+      if (L.phase == 0) {
         launch_step(step_args(h, L, rec), h->red_level, h->kind, h->stream);
         h->nlaunch++;
       }
+    // phase 1: rows next to an internal boundary, after this step's halo
+    bool any1 = false;
+    for (const Launch& L : h->launches) any1 |= L.phase == 1;
+    if (any1 && h->multi) {
+      if (p2p) {
+        const unsigned want = (unsigned)h->steps;  // neighbours finished step want-1
+        for (int side = 0; side < 2; ++side)
+          if (h->nbr[side].present &&
+              mo.wait32(h->stream, (unsigned long long)(h->flags + side), want, 0x0 /*GEQ*/))
+            return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
+      } else {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+      }
     }
+    for (const Launch& L : h->launches)
+      if (L.phase == 1) {
+        StepArgs a = step_args(h, L, rec);
+        if (p2p) set_remotes(h, L, a);
+        launch_step(a, h->red_level, h->kind, h->stream, p2p);
+        h->nlaunch++;
+      }
     CUDA_TRY(h, cudaGetLastError());
     if (h->multi) {
+      if (p2p) {  // tell the neighbours this step's rows have landed in their halos
+        const unsigned done = (unsigned)(h->steps + 1);
+        for (int side = 0; side < 2; ++side)
+          if (h->nbr[side].present &&
+              mo.write32(h->stream, (unsigned long long)(h->nbr[side].flags + (1 - side)), done,
+                         0x0))
+            return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
+      }
       CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
       if (h->red_level) {
-        h->pending_allreduce = true;
-        h->pending_step = h->steps;
+        if (p2p) {
+          CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+          int rc = nccl_allreduce_rec(h, rec, h->comm);
+          if (rc) return rc;
+        } else {
+          h->pending_allreduce = true;
+          h->pending_step = h->steps;
+        }
       }
     }
     h->cur = 1 - h->cur;
@@ -749,7 +897,9 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
                                 h->comm);
     if (rc) return rc;
     h->pending_allreduce = false;
-    // later work on the compute stream (reads of the history) follows the allreduce
+  }
+  if (h->multi && h->red_level) {
+    // later work on the compute stream (reads of the history) follows the allreduces
     CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
     CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
   }

@@ -66,8 +66,20 @@ struct RedArgs {
   double dxdy;
 };
 
+// Fused halo (P2P mode): output rows [lo, hi] (global, 1-based) are also
+// stored into a neighbour slab's state n+1 fields — another slab on this GPU
+// (virtual ranks) or a peer GPU's buffers mapped over NVLink (CUDA IPC).
+struct Remote {
+  float* En;
+  float* Un;
+  float* Vn;
+  long long jbase;   // the neighbour slab's global 1-based row of storage row 0
+  int lo, hi;        // rows to mirror; lo > hi: none
+};
+
 struct StepArgs {
   SlabView s;
+  Remote rem[2];             // used by the boundary launches in P2P halo mode
   int nx;
   long long ny;
   long long row_lo, row_hi;  // global 1-based output rows of this launch (inclusive)
@@ -84,7 +96,8 @@ struct StepArgs {
 // sharing one TMA row ring (default).
 int step_strips_per_cta(int kind);
 int step_grid(int kind, int nstrips, int nsegs);   // CTAs of one step launch
-void launch_step(const StepArgs& a, int red_level, int kind, void* stream);
+void launch_step(const StepArgs& a, int red_level, int kind, void* stream,
+                 bool remote = false);
 int step_occupancy_blocks_per_sm(int red_level, int kind);
 
 // set_state helper: checks finiteness of the interior, zeroes the wall faces

@@ -187,7 +187,23 @@ struct Ctx {
   unsigned umask;    // columns 1..nx-1 (faces that are not the east wall)
   int ny, ra, rb;    // global rows (1-based): grid rows, this segment's output rows
   bool out_lane;
+  int col;                 // storage column of this lane's element 0 (REMOTE only)
+  long long pitch;         // (REMOTE only)
+  const Remote* rem;       // (REMOTE only)
 };
+
+// P2P halo: mirror an output row into the neighbour slabs that need it
+__device__ __forceinline__ void remote_store(const Ctx& x, int field, int row, float a, float b,
+                                             float c, float d) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const Remote& m = x.rem[r];
+    if (row >= m.lo && row <= m.hi) {
+      float* base = field == 0 ? m.En : (field == 1 ? m.Un : m.Vn);
+      st4(base + (long long)(row - m.jbase) * x.pitch + x.col, a, b, c, d);
+    }
+  }
+}
 
 // the four byte-lanes of the result hold bits 0..3 of m (m < 16)
 __device__ __forceinline__ unsigned spread4(unsigned m) {
@@ -216,7 +232,7 @@ __device__ __forceinline__ float face(bool wc, bool wn, float d, float old) {
 }
 
 // One loaded row L: reads the window `w` (rows L-1, L-2), writes `o`.
-template <int RED>
+template <int RED, bool REMOTE>
 __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
                                          const float4 H4, const float4 U4,
                                          const float4 V4, const int L, const Ctx& x,
@@ -299,6 +315,7 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   if (x.out_lane) {
     if (in_rows(L, x.ra, x.rb)) {
       st4(pU, un[0], un[1], un[2], un[3]);
+      if (REMOTE) remote_store(x, 1, L, un[0], un[1], un[2], un[3]);
       if (RED >= 2) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(un[c]));
@@ -306,6 +323,7 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
     }
     if (in_rows(L - 1, x.ra, x.rb)) {
       st4(pV, vn[0], vn[1], vn[2], vn[3]);
+      if (REMOTE) remote_store(x, 2, L - 1, vn[0], vn[1], vn[2], vn[3]);
       if (RED >= 2) {
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vn[c]));
@@ -313,6 +331,7 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
     }
     if (in_rows(L - 2, x.ra, x.rb)) {
       st4(pE, En[0], En[1], En[2], En[3]);
+      if (REMOTE) remote_store(x, 0, L - 2, En[0], En[1], En[2], En[3]);
       if (RED >= 1) {
         // columns outside 1..nx hold exactly 0 (their etan is 0)
         acc.sum_eta += ((double)En[0] + (double)En[1]) + ((double)En[2] + (double)En[3]);
@@ -401,6 +420,7 @@ constexpr int kSmemPerWarp = kStages * kStageBytes;
 template <int RED>
 __global__ void __launch_bounds__(32 * kStepWarps)
     sw2d_step_warp(const StepArgs a) {
+  constexpr bool REMOTE = false;
   __shared__ __align__(128) unsigned char ring[kStepWarps][kSmemPerWarp];
   __shared__ __align__(8) unsigned long long bars[kStepWarps][kStages];
   const int lane = threadIdx.x & 31;
@@ -511,11 +531,11 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)i * pitch;
       fetch(i, E4, H4, U4, V4);
-      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
                     En + o - 2 * pitch);
       refill(i);
       fetch(i + 1, E4, H4, U4, V4);
-      row_step<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
+      row_step<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
                     En + o - pitch);
       refill(i + 1);
     }
@@ -523,7 +543,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)i * pitch;
       fetch(i, E4, H4, U4, V4);
-      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
                     En + o - 2 * pitch);
     }
   }
@@ -549,7 +569,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
-template <int RED>
+template <int RED, bool REMOTE>
 __global__ void __launch_bounds__(kCtaThreads, 1)
     sw2d_step_cta(const StepArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -624,6 +644,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+    x.col = c0;
+    x.pitch = pitch;
+    x.rem = a.rem;
 
     Win wa, wb;
 #pragma unroll
@@ -660,17 +683,17 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)i * pitch;
       fetch(i, E4, H4, U4, V4);
-      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
                     En + o - 2 * pitch);
       fetch(i + 1, E4, H4, U4, V4);
-      row_step<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
+      row_step<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
                     En + o - pitch);
     }
     if (i < n) {
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)i * pitch;
       fetch(i, E4, H4, U4, V4);
-      row_step<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
+      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
                     En + o - 2 * pitch);
     }
   }
@@ -757,24 +780,24 @@ int step_grid(int kind, int nstrips, int nsegs) {
 }
 
 namespace {
-template <int RED>
+template <int RED, bool REMOTE>
 void cta_attributes() {
-  cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(sw2d_step_cta<RED, REMOTE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kCtaSmem);
-  cudaFuncSetAttribute(sw2d_step_cta<RED>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       100);
+  cudaFuncSetAttribute(sw2d_step_cta<RED, REMOTE>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
-template <int RED>
+template <int RED, bool REMOTE>
 void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
   const int blocks = step_grid(kind, a.nstrips, a.nsegs);
-  if (kind == 1) {
+  if (kind == 1 || REMOTE) {
     static bool attr = false;  // per process: dynamic smem above 48 KB
     if (!attr) {
-      cta_attributes<RED>();
+      cta_attributes<RED, REMOTE>();
       attr = true;
     }
-    sw2d_step_cta<RED><<<blocks, kCtaThreads, kCtaSmem, s>>>(a);
+    sw2d_step_cta<RED, REMOTE><<<step_grid(1, a.nstrips, a.nsegs), kCtaThreads, kCtaSmem, s>>>(a);
   } else {
     sw2d_step_warp<RED><<<blocks, 32 * kStepWarps, 0, s>>>(a);
   }
@@ -784,8 +807,8 @@ template <int RED>
 int occupancy_kind(int kind) {
   int n = 0;
   if (kind == 1) {
-    cta_attributes<RED>();
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED>, kCtaThreads,
+    cta_attributes<RED, false>();
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED, false>, kCtaThreads,
                                                   kCtaSmem);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_warp<RED>, 32 * kStepWarps, 0);
@@ -794,14 +817,22 @@ int occupancy_kind(int kind) {
 }
 }  // namespace
 
-void launch_step(const StepArgs& a, int red_level, int kind, void* stream) {
+void launch_step(const StepArgs& a, int red_level, int kind, void* stream, bool remote) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (red_level >= 2)
-    launch_kind<2>(a, kind, s);
-  else if (red_level == 1)
-    launch_kind<1>(a, kind, s);
-  else
-    launch_kind<0>(a, kind, s);
+  if (remote) {
+    if (red_level >= 2)
+      launch_kind<2, true>(a, kind, s);
+    else if (red_level == 1)
+      launch_kind<1, true>(a, kind, s);
+    else
+      launch_kind<0, true>(a, kind, s);
+  } else if (red_level >= 2) {
+    launch_kind<2, false>(a, kind, s);
+  } else if (red_level == 1) {
+    launch_kind<1, false>(a, kind, s);
+  } else {
+    launch_kind<0, false>(a, kind, s);
+  }
 }
 
 int step_occupancy_blocks_per_sm(int red_level, int kind) {

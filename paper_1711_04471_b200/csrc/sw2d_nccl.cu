@@ -54,6 +54,7 @@ void load() {
             sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError) &&
             sym(h, "ncclSend", g_api.Send) && sym(h, "ncclRecv", g_api.Recv) &&
             sym(h, "ncclAllReduce", g_api.AllReduce) &&
+            sym(h, "ncclAllGather", g_api.AllGather) &&
             sym(h, "ncclGroupStart", g_api.GroupStart) &&
             sym(h, "ncclGroupEnd", g_api.GroupEnd) &&
             sym(h, "ncclGetErrorString", g_api.GetErrorString);
@@ -70,6 +71,29 @@ void load() {
 const NcclApi& nccl() {
   std::call_once(g_once, load);
   return g_api;
+}
+
+namespace {
+MemOps g_memops;
+std::once_flag g_memops_once;
+
+void load_memops() {
+  void* w = nullptr;
+  void* v = nullptr;
+  cudaDriverEntryPointQueryResult q1, q2;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &q2) != cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !v)
+    return;
+  g_memops.write32 = reinterpret_cast<decltype(g_memops.write32)>(w);
+  g_memops.wait32 = reinterpret_cast<decltype(g_memops.wait32)>(v);
+  g_memops.ok = true;
+}
+}  // namespace
+
+const MemOps& memops() {
+  std::call_once(g_memops_once, load_memops);
+  return g_memops;
 }
 
 }  // namespace sw2d_host

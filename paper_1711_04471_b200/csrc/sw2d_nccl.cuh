@@ -22,6 +22,8 @@ struct NcclApi {
                        cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t,
                             ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -29,5 +31,14 @@ struct NcclApi {
 
 // Loads once (thread-safe); returns the table (check .ok).
 const NcclApi& nccl();
+
+// CUDA driver stream memory operations (P2P halo signalling), resolved with
+// cudaGetDriverEntryPoint.  Values are 32-bit; wait is ">=".
+struct MemOps {
+  bool ok = false;
+  int (*write32)(cudaStream_t, unsigned long long addr, unsigned value, unsigned flags) = nullptr;
+  int (*wait32)(cudaStream_t, unsigned long long addr, unsigned value, unsigned flags) = nullptr;
+};
+const MemOps& memops();
 
 }  // namespace sw2d_host

@@ -25,6 +25,7 @@ SW2D_BC_CLOSED = 0
 SW2D_RED_N = 7
 SW2D_VARIANT_FUSED = 0
 SW2D_VARIANT_PAPER = 1
+SW2D_HALO_NCCL, SW2D_HALO_P2P = 0, 1
 
 #: every symbol include/sw2d.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",
@@ -52,7 +53,7 @@ class sw2d_params(ctypes.Structure):
 class sw2d_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("virtual_ranks", ctypes.c_int32),
-                ("nccl_id", ctypes.c_ubyte * 128)]
+                ("halo_mode", ctypes.c_int32), ("nccl_id", ctypes.c_ubyte * 128)]
 
 
 _lib = None
@@ -128,8 +129,9 @@ def make_params(nx, ny, dx=1.0, dy=1.0, dt=0.01, g=9.81, eps=0.05, hmin=0.05,
                        int(variant), int(history_len))
 
 
-def make_dist(rank=0, nranks=1, device=-1, virtual_ranks=0, nccl_id=None) -> sw2d_dist:
-    d = sw2d_dist(int(rank), int(nranks), int(device), int(virtual_ranks))
+def make_dist(rank=0, nranks=1, device=-1, virtual_ranks=0, nccl_id=None,
+              halo_mode=0) -> sw2d_dist:
+    d = sw2d_dist(int(rank), int(nranks), int(device), int(virtual_ranks), int(halo_mode))
     if nccl_id is not None:
         ctypes.memmove(d.nccl_id, bytes(nccl_id), 128)
     return d

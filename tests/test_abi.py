@@ -33,7 +33,9 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert sw2d.sw2d_abi_version() == 1
+    src = open(os.path.join(ROOT, "include", "sw2d.h")).read()
+    declared = int(re.search(r"#define SW2D_ABI_VERSION (\d+)", src).group(1))
+    assert sw2d.sw2d_abi_version() == declared
 
 
 def test_built_for_sm100a(lib):

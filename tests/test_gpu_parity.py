@@ -147,15 +147,19 @@ def test_fused_per_step_reductions(mask):
 
 # --- virtual ranks: the multi-GPU decomposition on one device -------------
 
+@pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
 @pytest.mark.parametrize("nranks", [2, 3, 5, 8])
-def test_virtual_ranks_bitwise_equal_single(nranks):
+def test_virtual_ranks_bitwise_equal_single(nranks, halo):
     """Row slabs with a 2-row halo exchanged every step reproduce the
     single-slab result bitwise (the per-cell arithmetic does not depend on
-    the slab), and the decomposed diagnostics agree."""
+    the slab), and the decomposed diagnostics agree.  HALO_NCCL moves the
+    halos with device copies between steps (the NCCL path's plan); HALO_P2P
+    has the boundary launches store their rows straight into the neighbour
+    slabs (the fused path real ranks run over NVLink)."""
     cfg, st = _bowl(263, 97)
     one, h1, r1, _ = gpu_run(P, st, 80, reduce_mask=ALL)
     many, hm, rm, _ = gpu_run(P, st, 80, reduce_mask=ALL,
-                              dist=sw2d.make_dist(0, nranks, virtual_ranks=1))
+                              dist=sw2d.make_dist(0, nranks, virtual_ranks=1, halo_mode=halo))
     assert_state_equal(many, one, where=f"{nranks} virtual ranks")
     want = oracle_run(P, st, 80)
     assert_state_equal(many, want, where=f"{nranks} virtual ranks vs oracle")
