@@ -59,6 +59,7 @@ struct sw2d {
   int nstrips = 0;
   int red_level = 0;
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
+  int tb_tw = 0, tb_th = 0, tb_k = 0;  // temporal blocking (small grids); tb_k = 0: off
   std::vector<Slab> slabs;
   std::vector<Launch> launches;
   int step_blocks = 0;
@@ -180,6 +181,30 @@ int red_level_of(uint32_t mask) {
 
 float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch; }
 
+// Small grids (the paper's 500^2 runs) are latency-bound.  Temporal blocking
+// (K steps per launch on shared-memory tiles) is opt-in (SW2D_TB=1): measured
+// slower than the per-step kernel on every paper size, kept
+// as a parity-tested experiment.
+constexpr long long kTbMaxCells = 1LL << 20;
+constexpr size_t kTbSmemMax = 200 * 1024;
+
+void plan_tb(sw2d* h, int sms) {
+  h->tb_k = 0;
+  const long long cells = h->p.nx * h->p.ny;
+  if (h->multi || h->virt || h->p.variant != SW2D_VARIANT_FUSED || h->red_level != 0) return;
+  if (cells > kTbMaxCells) return;
+  const char* on = std::getenv("SW2D_TB");
+  if (!on || std::atoi(on) == 0) return;
+  long long t = (long long)std::ceil(std::sqrt((double)cells / (double)sms));
+  t = std::max<long long>(8, std::min<long long>(t, 44));
+  int K = 8;
+  if (const char* e = std::getenv("SW2D_TB_K")) K = std::max(1, std::min(16, std::atoi(e)));
+  while (K > 1 && tb_smem_bytes((int)t, (int)t, K) > kTbSmemMax) --K;
+  if (K < 2) return;
+  h->tb_tw = h->tb_th = (int)t;
+  h->tb_k = K;
+}
+
 void plan_launches(sw2d* h) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -222,7 +247,11 @@ void plan_launches(sw2d* h) {
     if (hi_halo) add(s, J1 - 1, J1, 1);
   }
   h->step_blocks = part;
+  plan_tb(h, sms);
   if (std::getenv("SW2D_VERBOSE")) {
+    if (h->tb_k)
+      std::fprintf(stderr, "[sw2d] temporal blocking: %dx%d tiles, %d steps per launch\n",
+                   h->tb_tw, h->tb_th, h->tb_k);
     std::fprintf(stderr, "[sw2d] kind %d red %d: %d CTAs/SM on %d SMs, %d strips\n", h->kind,
                  h->red_level, bps, sms, h->nstrips);
     for (const Launch& L : h->launches)
@@ -816,6 +845,36 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
         if (rc) return rc;
       }
       h->steps++;
+    }
+    return SW2D_OK;
+  }
+  if (h->tb_k) {  // temporally blocked: K steps per launch
+    Slab& sl = h->slabs[0];
+    int64_t left = nsteps;
+    while (left > 0) {
+      const int k = (int)std::min<int64_t>(left, h->tb_k);
+      TbArgs a;
+      a.E = sl.E[h->cur];
+      a.U = sl.U[h->cur];
+      a.V = sl.V[h->cur];
+      a.H0 = sl.H0;
+      a.En = sl.E[1 - h->cur];
+      a.Un = sl.U[1 - h->cur];
+      a.Vn = sl.V[1 - h->cur];
+      a.pitch = h->pitch;
+      a.jbase = sl.j0 + 1 - kHaloRows;
+      a.nx = (int)h->p.nx;
+      a.ny = (int)h->p.ny;
+      a.tw = h->tb_tw;
+      a.th = h->tb_th;
+      a.K = k;
+      a.c = h->coef;
+      launch_tb(a, h->stream);
+      h->nlaunch++;
+      CUDA_TRY(h, cudaGetLastError());
+      h->cur = 1 - h->cur;
+      h->steps += k;
+      left -= k;
     }
     return SW2D_OK;
   }

@@ -160,6 +160,25 @@ struct PaperArgs {
 void launch_paper_step(const PaperArgs& a, void* stream);   // 3 launches
 void launch_paper_init(const PaperArgs& a, void* stream);   // h, wet_out from H0 + E
 
+// Temporally blocked steps for small grids (sw2d_tb_kernels.cu): K steps per
+// launch on tw x th tiles with a 2K-cell apron in shared memory.
+struct TbArgs {
+  const float* E;
+  const float* U;
+  const float* V;
+  const float* H0;
+  float* En;
+  float* Un;
+  float* Vn;
+  long long pitch;
+  long long jbase;
+  int nx, ny;
+  int tw, th, K;
+  Coef c;
+};
+size_t tb_smem_bytes(int tw, int th, int K);
+void launch_tb(const TbArgs& a, void* stream);
+
 // wet mask of the current state into a dense uint8 [nrows][nx] buffer.
 void launch_wet(const float* E, const float* H0, long long pitch,
                 long long nrows, int nx, float hmin, unsigned char* out,

@@ -337,3 +337,20 @@ def _random_state(nx, ny):
     u = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
     v = rng.uniform(-0.3, 0.3, (ny, nx)).astype(np.float32)
     return hz, e, u, v
+
+
+# --- temporally blocked small-grid path (NEXT-2) ---------------------------
+
+@pytest.mark.parametrize("nx,ny,n,k", [(500, 500, 100, "8"), (100, 100, 37, "8"), (263, 97, 50, "3"),
+                                       (1, 1, 9, "8"), (7, 300, 20, "2"), (1000, 1000, 16, "8")])
+def test_temporal_blocking_bitwise(nx, ny, n, k, monkeypatch):
+    """K steps per launch on shared-memory tiles with a 2K apron equal the
+    oracle bitwise (and hence the per-step kernel), including a step count
+    that is not a multiple of K."""
+    st = _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny)
+    monkeypatch.setenv("SW2D_TB", "1")
+    monkeypatch.setenv("SW2D_TB_K", k)
+    got, _, _, launches = gpu_run(P, st, n)
+    want = oracle_run(P, st, n)
+    assert_state_equal(got, want, where=f"temporal blocking {nx}x{ny} K={k}")
+    assert launches < n + 8   # K steps per launch (+ set_state / reduce helpers)
