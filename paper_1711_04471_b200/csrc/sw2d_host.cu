@@ -98,6 +98,7 @@ struct sw2d {
     float* V[2] = {nullptr, nullptr};
     unsigned int* flags = nullptr;
     long long jbase = 0;
+    long long nelem = 0;
   } nbr[2];                       // [0]: south (rank-1), [1]: north (rank+1); IPC-mapped
 };
 
@@ -272,6 +273,7 @@ StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
   a.s.Vn = sl.V[1 - h->cur];
   a.s.pitch = h->pitch;
   a.s.jbase = sl.j0 + 1 - kHaloRows;
+  a.s.nelem = (sl.nrows + 2 * kHaloRows) * h->pitch;
   a.nx = (int)h->p.nx;
   a.ny = h->p.ny;
   a.row_lo = L.row_lo;
@@ -303,23 +305,26 @@ void set_remotes(sw2d* h, const Launch& L, StepArgs& a) {
   const int nb = 1 - h->cur;  // the buffer being written this step
   for (int side = 0; side < 2; ++side) {
     float *E = nullptr, *U = nullptr, *V = nullptr;
-    long long jb = 0;
+    long long jb = 0, ne = 0;
     if (h->virt) {
       const int peer = L.slab + (side == 0 ? -1 : 1);
       if (peer < 0 || peer >= (int)h->slabs.size()) continue;
       const Slab& ps = h->slabs[peer];
       E = ps.E[nb]; U = ps.U[nb]; V = ps.V[nb];
       jb = ps.j0 + 1 - kHaloRows;
+      ne = (ps.nrows + 2 * kHaloRows) * h->pitch;
     } else {
       const auto& pr = h->nbr[side];
       if (!pr.present) continue;
       E = pr.E[nb]; U = pr.U[nb]; V = pr.V[nb];
       jb = pr.jbase;
+      ne = pr.nelem;
     }
     a.rem[side].En = E;
     a.rem[side].Un = U;
     a.rem[side].Vn = V;
     a.rem[side].jbase = jb;
+    a.rem[side].nelem = ne;
     a.rem[side].lo = (int)(side == 0 ? J0 : J1 - 1);
     a.rem[side].hi = (int)(side == 0 ? J0 + 1 : J1);
   }
@@ -547,6 +552,7 @@ int setup_p2p(sw2d* h) {
     int64_t j0, nrows;
     sw2d_partition(h->p.ny, h->nranks, peer, &j0, &nrows);
     pr.jbase = j0 + 1 - kHaloRows;
+    pr.nelem = (nrows + 2 * kHaloRows) * h->pitch;
     pr.present = true;
   }
   return SW2D_OK;

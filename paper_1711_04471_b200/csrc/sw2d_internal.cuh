@@ -11,6 +11,7 @@
 // written by two warps.  pitch is a multiple of 32 floats (128 B).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 
 namespace sw2d_dev {
 
@@ -42,7 +43,25 @@ struct SlabView {
   float* Vn;
   long long pitch;   // floats per storage row
   long long jbase;   // global 1-based row of storage row 0
+  long long nelem;   // floats per field allocation (bounds checks in debug builds)
 };
+
+// Debug builds (python -m paper_1711_04471_b200._build --debug): every global
+// store and TMA window of the step kernels is bounds-checked on the device.
+#ifdef SW2D_DEBUG_BOUNDS
+#define SW2D_CHECK(cond)                                                     \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      printf("sw2d bounds check failed: %s (%s:%d) block %d thread %d\n",    \
+             #cond, __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x);   \
+      __trap();                                                              \
+    }                                                                        \
+  } while (0)
+#else
+#define SW2D_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // Per-step diagnostics record (7 doubles, see SW2D_RED_*): the sum part
 // [0..2] and the max part [3..6] are allreduced separately across ranks.
@@ -74,6 +93,7 @@ struct Remote {
   float* Un;
   float* Vn;
   long long jbase;   // the neighbour slab's global 1-based row of storage row 0
+  long long nelem;   // floats per field of the neighbour slab (debug bounds checks)
   int lo, hi;        // rows to mirror; lo > hi: none
 };
 

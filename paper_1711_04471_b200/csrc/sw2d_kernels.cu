@@ -190,6 +190,12 @@ struct Ctx {
   int col;                 // storage column of this lane's element 0 (REMOTE only)
   long long pitch;         // (REMOTE only)
   const Remote* rem;       // (REMOTE only)
+#ifdef SW2D_DEBUG_BOUNDS
+  const float* dU;         // field bases and size for the bounds checks
+  const float* dV;
+  const float* dE;
+  long long nelem;
+#endif
 };
 
 // P2P halo: mirror an output row into the neighbour slabs that need it
@@ -200,6 +206,7 @@ __device__ __forceinline__ void remote_store(const Ctx& x, int field, int row, f
     const Remote& m = x.rem[r];
     if (row >= m.lo && row <= m.hi) {
       float* base = field == 0 ? m.En : (field == 1 ? m.Un : m.Vn);
+      SW2D_CHECK(row - m.jbase >= 0 && (row - m.jbase) * x.pitch + x.col + 4 <= m.nelem);
       st4(base + (long long)(row - m.jbase) * x.pitch + x.col, a, b, c, d);
     }
   }
@@ -314,6 +321,9 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   // a5: commit (lanes 1..30, rows of this segment)
   if (x.out_lane) {
     if (in_rows(L, x.ra, x.rb)) {
+#ifdef SW2D_DEBUG_BOUNDS
+      SW2D_CHECK(pU >= x.dU && pU + 4 <= x.dU + x.nelem);
+#endif
       st4(pU, un[0], un[1], un[2], un[3]);
       if (REMOTE) remote_store(x, 1, L, un[0], un[1], un[2], un[3]);
       if (RED >= 2) {
@@ -322,6 +332,9 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
       }
     }
     if (in_rows(L - 1, x.ra, x.rb)) {
+#ifdef SW2D_DEBUG_BOUNDS
+      SW2D_CHECK(pV >= x.dV && pV + 4 <= x.dV + x.nelem);
+#endif
       st4(pV, vn[0], vn[1], vn[2], vn[3]);
       if (REMOTE) remote_store(x, 2, L - 1, vn[0], vn[1], vn[2], vn[3]);
       if (RED >= 2) {
@@ -330,6 +343,9 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
       }
     }
     if (in_rows(L - 2, x.ra, x.rb)) {
+#ifdef SW2D_DEBUG_BOUNDS
+      SW2D_CHECK(pE >= x.dE && pE + 4 <= x.dE + x.nelem);
+#endif
       st4(pE, En[0], En[1], En[2], En[3]);
       if (REMOTE) remote_store(x, 0, L - 2, En[0], En[1], En[2], En[3]);
       if (RED >= 1) {
@@ -449,6 +465,12 @@ __global__ void __launch_bounds__(32 * kStepWarps)
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+#ifdef SW2D_DEBUG_BOUNDS
+    x.dU = a.s.Un;
+    x.dV = a.s.Vn;
+    x.dE = a.s.En;
+    x.nelem = a.s.nelem;
+#endif
     const long long pitch = a.s.pitch;
 
     const int first = x.ra - 2;      // first loaded row
@@ -468,6 +490,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       for (int st = 0; st < kStages; ++st) {
         if (first + st <= last) {
           const long long o = off0 + st * pitch;
+          SW2D_CHECK(o >= 0 && o + kRowBytes / 4 <= a.s.nelem);
           const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
           mbar_expect_tx(b, kStageBytes);
           bulk_g2s(d, a.s.E + o, kRowBytes, b);
@@ -514,6 +537,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       if (lane == 0 && r <= last) {
         const int st = i & (kStages - 1);
         const long long o = off0 + (long long)(i + kStages) * pitch;
+        SW2D_CHECK(o >= 0 && o + kRowBytes / 4 <= a.s.nelem);
         const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
         fence_proxy_async();
         mbar_expect_tx(b, kStageBytes);
@@ -619,6 +643,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
           }
         }
         const long long o = off0 + (long long)r * pitch;
+        SW2D_CHECK(o >= 0 && o + wb / 4 <= a.s.nelem);
         const uint32_t d = sring + st * kCtaStageBytes, b = sfull + 8 * st;
         mbar_expect_tx(b, 4u * wb);
         bulk_g2s(d, a.s.E + o, wb, b);
@@ -644,6 +669,12 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+#ifdef SW2D_DEBUG_BOUNDS
+    x.dU = a.s.Un;
+    x.dV = a.s.Vn;
+    x.dE = a.s.En;
+    x.nelem = a.s.nelem;
+#endif
     x.col = c0;
     x.pitch = pitch;
     x.rem = a.rem;

@@ -15,7 +15,8 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsw2d.so")
+_LIB_PATH = os.environ.get("SW2D_LIBRARY") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libsw2d.so")   # SW2D_LIBRARY: debug build
 
 SW2D_OK, SW2D_EINVAL, SW2D_ENOMEM, SW2D_ECUDA, SW2D_ENCCL, SW2D_ESTATE, \
     SW2D_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6

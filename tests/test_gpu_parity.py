@@ -354,3 +354,45 @@ def test_temporal_blocking_bitwise(nx, ny, n, k, monkeypatch):
     want = oracle_run(P, st, n)
     assert_state_equal(got, want, where=f"temporal blocking {nx}x{ny} K={k}")
     assert launches < n + 8   # K steps per launch (+ set_state / reduce helpers)
+
+
+def test_c4_max_size_single_gpu_sampled_parity():
+    """The largest BASELINE grid, C4 32768^2 (30 GB of state), on one GPU:
+    inputs built on the device chunk by chunk, state uploaded from CUDA
+    memory (UVA), sampled windows checked against the oracle."""
+    import torch
+    cfg = si.config("c4")
+    nx, ny, n = cfg["nx"], cfg["ny"], 6
+    dev = [torch.empty((ny, nx), dtype=torch.float32, device="cuda") for _ in range(4)]
+    step = 2048
+    for j0 in range(0, ny, step):
+        part = si.generate(cfg, j0=j0, nrows=min(step, ny - j0))
+        for d, a in zip(dev, part):
+            d[j0:j0 + a.shape[0]].copy_(torch.from_numpy(a))
+    p = sw2d.make_params(nx, ny)
+    h = sw2d.sw2d_create(p, None, torch.cuda.current_stream())
+    try:
+        sw2d.sw2d_set_state(h, *dev)
+        v0 = sw2d.sw2d_reduce(h, sw2d.SW2D_RED_VOLUME)
+        sw2d.sw2d_step(h, n)
+        out = [torch.empty_like(dev[0]) for _ in range(3)]
+        wet = torch.empty((ny, nx), dtype=torch.uint8, device="cuda")
+        sw2d.sw2d_get_state(h, *out, wet)
+        v1 = sw2d.sw2d_reduce(h, sw2d.SW2D_RED_VOLUME)
+    finally:
+        sw2d.sw2d_destroy(h)
+    del dev
+    size, m = 32, 2 * n + 2
+    centers = [(0, 0), (ny - 1, nx - 1), (ny // 2, nx // 2), (ny // 3, 2 * nx // 3),
+               (0, nx // 2), (ny - 1, 17)]
+    for (jc, kc) in centers:
+        j0 = min(max(jc - size // 2, 0), ny - size)
+        k0 = min(max(kc - size // 2, 0), nx - size)
+        wj0, wk0 = max(j0 - m, 0), max(k0 - m, 0)
+        wj1, wk1 = min(j0 + size + m, ny), min(k0 + size + m, nx)
+        st = si.generate(cfg, j0=wj0, nrows=wj1 - wj0, k0=wk0, ncols=wk1 - wk0)
+        want = oracle_run(P, st, n)
+        sl = (slice(j0 - wj0, j0 - wj0 + size), slice(k0 - wk0, k0 - wk0 + size))
+        sub = [t[j0:j0 + size, k0:k0 + size].cpu().numpy() for t in (*out, wet)]
+        assert_state_equal(sub, [w[sl] for w in want], where=f"C4 window ({j0},{k0})")
+    assert abs(v1 - v0) <= 1e-6 * v0
