@@ -60,6 +60,9 @@ def parse():
                     help="paper: the paper-shaped 3-map-kernel step (NEXT-1, comparison)")
     ap.add_argument("--halo", choices=["nccl", "p2p"], default="nccl",
                     help="N>1 halo exchange: NCCL send/recv, or fused P2P stores (IPC)")
+    ap.add_argument("--snapshots", action="store_true",
+                    help="also time sw2d_run_snapshots: eta to pinned host memory once per "
+                         "bench step, the copy overlapped with the next steps (NEXT-3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -306,6 +309,23 @@ def run_ours(args, cfg, ws, rank, local):
                 "note": "per-model-step time of the whole timed region (the step kernel "
                         "is the only kernel per step; its fused last-CTA fold included)"}
 
+        # --- periodic output overlapped with compute (optional) ------------
+        snaps = None
+        if args.snapshots:
+            snapbuf = torch.empty((1, nrows, nx), dtype=torch.float32, pin_memory=True)
+            barrier()
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            for _ in range(args.steps):
+                sw2d.sw2d_run_snapshots(h, T, T, snapbuf)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            sms = max_over_ranks(s0.elapsed_time(s1))
+            snaps = {"value": nx * ny * T * args.steps / (sms * 1e-3), "unit": UNIT,
+                     "every": T, "d2h_bytes_per_step": 4 * cells_local,
+                     "path": "sw2d_run_snapshots(T, every=T) per bench step, pinned host"}
+
         # --- e2e: host buffers through the C ABI ----------------------------
         e2e = None
         if not args.no_e2e and not args.profile:
@@ -361,6 +381,8 @@ def run_ours(args, cfg, ws, rank, local):
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "clocks": clk.summary(), "gpu_launches": launches,
     }
+    if snaps is not None:
+        line["snapshots"] = snaps
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

@@ -168,6 +168,17 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
  * allreduces the per-step diagnostics. */
 int sw2d_step(sw2d* h, int64_t nsteps);
 
+/* Periodic output (the paper's once-per-run / per-iteration transfer
+ * scheduling): run nsteps steps and
+ * deliver eta after every `every` steps: out_eta[k] ([nrows][nx] float32, the
+ * rows this handle holds) = eta after (k+1)*every steps, k < nsnap =
+ * nsteps / every.  Each snapshot is packed on the device into one of two
+ * staging buffers and copied to the host on a copy stream while the following
+ * steps run (use pinned host memory for the overlap).  Synchronizes before
+ * returning.  SW2D_EINVAL if every < 1 or nsnap != nsteps / every. */
+int sw2d_run_snapshots(sw2d* h, int64_t nsteps, int64_t every, float* out_eta,
+                       int64_t nsnap);
+
 /* The global value of diagnostic `op` (SW2D_RED_*) of the current state, on
  * every rank.  Synchronizes. */
 int sw2d_reduce(sw2d* h, int op, double* out);

@@ -79,6 +79,10 @@ struct sw2d {
   int* bad = nullptr;
   unsigned char* wetbuf = nullptr;
   size_t wetbuf_bytes = 0;
+  float* snap[2] = {nullptr, nullptr};   // periodic-output staging buffers
+  size_t snap_bytes = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_snap[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   int64_t steps = 0;
   int wcur = 0;  // paper variant: current wet buffer
   bool state_set = false;
@@ -493,6 +497,13 @@ void free_all(sw2d* h) {
   cudaFree(h->zero);
   cudaFree(h->bad);
   cudaFree(h->wetbuf);
+  cudaFree(h->snap[0]);
+  cudaFree(h->snap[1]);
+  for (int b = 0; b < 2; ++b) {
+    if (h->ev_snap[b]) cudaEventDestroy(h->ev_snap[b]);
+    if (h->ev_copied[b]) cudaEventDestroy(h->ev_copied[b]);
+  }
+  if (h->copy) cudaStreamDestroy(h->copy);
   if (h->ev_ready) cudaEventDestroy(h->ev_ready);
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);
   if (h->comm) cudaStreamDestroy(h->comm);
@@ -968,6 +979,59 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
     CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
     CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
   }
+  return SW2D_OK;
+}
+
+int sw2d_run_snapshots(sw2d* h, int64_t nsteps, int64_t every, float* out_eta,
+                       int64_t nsnap) {
+  ENTER(h);
+  if (!out_eta || every < 1 || nsteps < 0 || nsnap != nsteps / every)
+    return fail(h, SW2D_EINVAL, "need every >= 1, nsnap == nsteps / every, out_eta");
+  if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_run_snapshots before sw2d_set_state");
+  const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
+  int64_t rows = 0;
+  for (Slab& s : h->slabs) rows += s.nrows;
+  const size_t bytes = (size_t)rows * (size_t)nx * sizeof(float);
+  if (bytes > h->snap_bytes) {
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(h->snap[b]);
+      h->snap[b] = nullptr;
+    }
+    h->snap_bytes = 0;
+    for (int b = 0; b < 2; ++b) CUDA_TRY(h, cudaMalloc(&h->snap[b], bytes));
+    h->snap_bytes = bytes;
+  }
+  if (!h->copy) {
+    CUDA_TRY(h, cudaStreamCreateWithFlags(&h->copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_snap[b], cudaEventDisableTiming));
+      CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_copied[b], cudaEventDisableTiming));
+    }
+  }
+  const size_t wbytes = (size_t)nx * sizeof(float);
+  const size_t dp = (size_t)h->pitch * sizeof(float);
+  for (int64_t k = 0; k < nsnap; ++k) {
+    int rc = sw2d_step(h, every);
+    if (rc) return rc;
+    const int b = (int)(k & 1);
+    if (k >= 2) CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_copied[b], 0));
+    for (Slab& s : h->slabs)  // pack the interior of eta (device to device)
+      CUDA_TRY(h, cudaMemcpy2DAsync(h->snap[b] + (size_t)(s.j0 - hj0) * (size_t)nx, wbytes,
+                                    s.E[h->cur] + kHaloRows * h->pitch + 1 + kColOff, dp,
+                                    wbytes, (size_t)s.nrows, cudaMemcpyDeviceToDevice,
+                                    h->stream));
+    CUDA_TRY(h, cudaEventRecord(h->ev_snap[b], h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->copy, h->ev_snap[b], 0));
+    CUDA_TRY(h, cudaMemcpyAsync(out_eta + (size_t)k * (size_t)rows * (size_t)nx, h->snap[b],
+                                bytes, cudaMemcpyDefault, h->copy));
+    CUDA_TRY(h, cudaEventRecord(h->ev_copied[b], h->copy));
+  }
+  {
+    int rc = sw2d_step(h, nsteps - nsnap * every);
+    if (rc) return rc;
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(h->copy));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   return SW2D_OK;
 }
 

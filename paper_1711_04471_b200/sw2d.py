@@ -31,7 +31,8 @@ SW2D_HALO_NCCL, SW2D_HALO_P2P = 0, 1
 #: every symbol include/sw2d.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",
            "sw2d_create", "sw2d_local_rows", "sw2d_set_state", "sw2d_step",
-           "sw2d_reduce", "sw2d_reduce_history", "sw2d_get_state", "sw2d_sync",
+           "sw2d_run_snapshots", "sw2d_reduce", "sw2d_reduce_history", "sw2d_get_state",
+           "sw2d_sync",
            "sw2d_launch_count", "sw2d_destroy", "sw2d_strerror",
            "sw2d_last_error")
 
@@ -81,6 +82,7 @@ def load(path: str = _LIB_PATH):
         "sw2d_local_rows": ([vp, p64, p64], ctypes.c_int),
         "sw2d_set_state": ([vp, vp, vp, vp, vp], ctypes.c_int),
         "sw2d_step": ([vp, i64], ctypes.c_int),
+        "sw2d_run_snapshots": ([vp, i64, i64, vp, i64], ctypes.c_int),
         "sw2d_reduce": ([vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
         "sw2d_reduce_history": ([vp, ctypes.c_int, vp, i64], ctypes.c_int),
         "sw2d_get_state": ([vp, vp, vp, vp, vp], ctypes.c_int),
@@ -196,6 +198,14 @@ def sw2d_set_state(h, hzero, eta, u=None, v=None) -> None:
 
 def sw2d_step(h, nsteps: int) -> None:
     _check(load().sw2d_step(h, int(nsteps)), h)
+
+
+def sw2d_run_snapshots(h, nsteps: int, every: int, out_eta) -> None:
+    """Run nsteps; out_eta [nsnap][nrows][nx] float32 receives eta after every
+    `every` steps (nsnap = nsteps // every)."""
+    nsnap = int(nsteps) // int(every) if every else -1
+    _check(load().sw2d_run_snapshots(h, int(nsteps), int(every), _ptr(out_eta, writable=True),
+                                     nsnap), h)
 
 
 def sw2d_reduce(h, op: int) -> float:

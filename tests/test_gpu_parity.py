@@ -396,3 +396,33 @@ def test_c4_max_size_single_gpu_sampled_parity():
         sub = [t[j0:j0 + size, k0:k0 + size].cpu().numpy() for t in (*out, wet)]
         assert_state_equal(sub, [w[sl] for w in want], where=f"C4 window ({j0},{k0})")
     assert abs(v1 - v0) <= 1e-6 * v0
+
+
+# --- periodic output (NEXT-3) ----------------------------------------------
+
+@pytest.mark.parametrize("dist", [None, "virtual3"])
+def test_snapshots_equal_oracle_states(dist):
+    """sw2d_run_snapshots delivers eta after every `every` steps (copies
+    overlapped with the following steps); each snapshot equals the oracle's
+    state at that step bitwise, and the final state is that of nsteps."""
+    import torch
+    cfg, st = _bowl(301, 203)
+    ny, nx = st[0].shape
+    nsteps, every = 40, 7
+    nsnap = nsteps // every
+    out = torch.empty((nsnap, ny, nx), dtype=torch.float32, pin_memory=True)
+    d = sw2d.make_dist(0, 3, virtual_ranks=1) if dist else None
+    h = sw2d.sw2d_create(sw2d.make_params(nx, ny), d)
+    try:
+        sw2d.sw2d_set_state(h, *st)
+        sw2d.sw2d_run_snapshots(h, nsteps, every, out)
+        final = sw2d.get_state(h, nx)
+    finally:
+        sw2d.sw2d_destroy(h)
+    cur = st
+    for k in range(nsnap):
+        e, u, v = oracle.run(P, cur[0], cur[1], cur[2], cur[3], every)
+        cur = (cur[0], e, u, v)
+        np.testing.assert_array_equal(out[k].numpy(), e)
+    e, u, v = oracle.run(P, cur[0], cur[1], cur[2], cur[3], nsteps - nsnap * every)
+    assert_state_equal(final[:3] + (None,), (e, u, v, None), where="after snapshots")
