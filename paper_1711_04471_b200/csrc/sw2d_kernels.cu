@@ -823,10 +823,12 @@ template <int RED, bool REMOTE>
 void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
   const int blocks = step_grid(kind, a.nstrips, a.nsegs);
   if (kind == 1 || REMOTE) {
-    static bool attr = false;  // per process: dynamic smem above 48 KB
-    if (!attr) {
+    static unsigned long long attr_devices = 0;  // dynamic smem above 48 KB, per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_devices >> (dev & 63) & 1ull)) {
       cta_attributes<RED, REMOTE>();
-      attr = true;
+      attr_devices |= 1ull << (dev & 63);
     }
     sw2d_step_cta<RED, REMOTE><<<step_grid(1, a.nstrips, a.nsegs), kCtaThreads, kCtaSmem, s>>>(a);
   } else {

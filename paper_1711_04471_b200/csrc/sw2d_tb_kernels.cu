@@ -185,10 +185,12 @@ size_t tb_smem_bytes(int tw, int th, int K) {
 }
 
 void launch_tb(const TbArgs& a, void* stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr_devices = 0;  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_devices >> (dev & 63) & 1ull)) {
     cudaFuncSetAttribute(sw2d_step_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
+    attr_devices |= 1ull << (dev & 63);
   }
   const dim3 grid((unsigned)((a.nx + a.tw - 1) / a.tw), (unsigned)((a.ny + a.th - 1) / a.th));
   sw2d_step_tb<<<grid, dim3(kTbX, kTbY), tb_smem_bytes(a.tw, a.th, a.K),
