@@ -576,6 +576,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   h->coef = make_coef(h->p);
   if (const char* k = std::getenv("SW2D_STEP_KERNEL")) h->kind = std::atoi(k) == 0 ? 0 : 1;
   h->red_level = red_level_of(h->p.reduce_every_step);
+  if (const char* e = std::getenv("SW2D_MIN_RED")) h->red_level = std::max(h->red_level, std::atoi(e));
   h->hist_len = h->p.history_len;
   if (dist) {
     if (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks)

@@ -583,6 +583,10 @@ __global__ void __launch_bounds__(32 * kStepWarps)
 // The compute warps wait on `full`, copy their float4 of each field out of
 // the stage and release it on `empty` (one arrival per compute warp).
 constexpr int kCtaStrips = 8;
+#ifndef SW2D_CTA_EXIT_BARRIER
+#define SW2D_CTA_EXIT_BARRIER 1
+#endif
+constexpr bool kCtaBarrierAtExit = SW2D_CTA_EXIT_BARRIER;
 constexpr int kCtaStages = 6;
 constexpr int kCtaWinBytes = (kCtaStrips * kColsPerStrip + 8) * 4;   // one field, one row
 constexpr int kCtaStageBytes = 4 * kCtaWinBytes;
@@ -728,7 +732,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                     En + o - 2 * pitch);
     }
   }
-  if (RED >= 1) block_reduce_and_finalize<RED, kCtaStrips + 1>(acc, a.red);
+  if (RED >= 1) {
+    block_reduce_and_finalize<RED, kCtaStrips + 1>(acc, a.red);
+  } else if (kCtaBarrierAtExit) {
+    __syncthreads();  // keep the producer warp resident until the compute warps finish
+  }
 }
 
 // ---------------------------------------------------------------------------
