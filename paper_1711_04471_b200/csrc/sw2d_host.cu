@@ -26,6 +26,7 @@ namespace {
 
 thread_local std::string t_create_err;
 
+constexpr long long kSmallMaxCells = 1LL << 22;   // small-grid kernel up to 2048^2
 constexpr int kMinRowsPerSeg = 4;   // small grids: more, shorter segments (latency-bound)
 constexpr int kDefaultHistory = 1024;
 
@@ -63,6 +64,8 @@ struct sw2d {
   std::vector<Slab> slabs;
   std::vector<Launch> launches;
   int step_blocks = 0;
+  Launch two{};          // two steps per launch (one slab): its single launch
+  bool two_ok = false;
   int cur = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -253,6 +256,27 @@ void plan_launches(sw2d* h) {
   }
   h->step_blocks = part;
   plan_tb(h, sms);
+  // two steps per launch: one slab, the CTA kernel, no P2P halo
+  h->two_ok = false;
+  const char* two_env = std::getenv("SW2D_TWO_STEP");
+  if (!h->multi && !h->virt && h->kind == 1 && h->p.variant == SW2D_VARIANT_FUSED &&
+      h->halo_mode != SW2D_HALO_P2P && !(two_env && std::atoi(two_env) == 0)) {
+    const int per2 = step2_strips_per_cta();
+    const long long ncc2 = (h->nstrips + per2 - 1) / per2;
+    const long long segs2 = std::max(1LL, (long long)sms / ncc2);
+    const long long rows = h->p.ny;
+    long long rps = std::max<long long>((rows + segs2 - 1) / segs2, 8);
+    Launch& L = h->two;
+    L.slab = 0;
+    L.row_lo = 1;
+    L.row_hi = rows;
+    L.rows_per_seg = (int)rps;
+    L.nsegs = (int)((rows + rps - 1) / rps);
+    L.blocks = (int)(ncc2 * L.nsegs);
+    L.part_base = 0;
+    L.phase = 0;
+    h->two_ok = true;
+  }
   if (std::getenv("SW2D_VERBOSE")) {
     if (h->tb_k)
       std::fprintf(stderr, "[sw2d] temporal blocking: %dx%d tiles, %d steps per launch\n",
@@ -262,6 +286,9 @@ void plan_launches(sw2d* h) {
     for (const Launch& L : h->launches)
       std::fprintf(stderr, "[sw2d]   slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
                    L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
+    if (h->two_ok)
+      std::fprintf(stderr, "[sw2d]   two steps per launch: %d segs x %d rows, %d CTAs\n",
+                   h->two.nsegs, h->two.rows_per_seg, h->two.blocks);
   }
 }
 
@@ -574,7 +601,6 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   h->p = *params;
   if (h->p.history_len == 0) h->p.history_len = kDefaultHistory;
   h->coef = make_coef(h->p);
-  if (const char* k = std::getenv("SW2D_STEP_KERNEL")) h->kind = std::atoi(k) == 0 ? 0 : 1;
   h->red_level = red_level_of(h->p.reduce_every_step);
   if (const char* e = std::getenv("SW2D_MIN_RED")) h->red_level = std::max(h->red_level, std::atoi(e));
   h->hist_len = h->p.history_len;
@@ -588,7 +614,6 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     if (dist->halo_mode != SW2D_HALO_NCCL && dist->halo_mode != SW2D_HALO_P2P)
       return fail(h, SW2D_EINVAL, "unknown halo_mode");
     h->halo_mode = dist->halo_mode;
-    if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
     if (dist->device >= 0) CUDA_TRY(h, cudaSetDevice(dist->device));
   }
   CUDA_TRY(h, cudaGetDevice(&h->device));
@@ -608,8 +633,17 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
       return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 4 rows per rank)");
     h->slabs.push_back(s);
   }
-  h->nstrips = (int)((h->p.nx + kColsPerStrip - 1) / kColsPerStrip);
-  const int64_t need = (int64_t)h->nstrips * kColsPerStrip + kStripBase + 8;
+  // kernel kind: the CTA/TMA kernel, or the small-grid kernel for grids that
+  // are L2-resident and latency-bound (SW2D_STEP_KERNEL overrides)
+  if (h->halo_mode != SW2D_HALO_P2P && h->p.nx * h->p.ny <= kSmallMaxCells) h->kind = 2;
+  if (const char* k = std::getenv("SW2D_STEP_KERNEL")) {
+    const int v = std::atoi(k);
+    h->kind = (v == 0 || v == 2) ? v : 1;
+  }
+  if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
+  const int64_t strips4 = (h->p.nx + kColsPerStrip - 1) / kColsPerStrip;
+  h->nstrips = (int)((h->p.nx + step_strip_cols(h->kind) - 1) / step_strip_cols(h->kind));
+  const int64_t need = strips4 * kColsPerStrip + kStripBase + 8;  // covers both layouts
   h->pitch = (need + 31) / 32 * 32;
   // streams
   if (cuda_stream) {
@@ -641,7 +675,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   }
   plan_launches(h);
   // reduction scratch
-  long long cap = h->step_blocks;
+  long long cap = std::max<long long>(h->step_blocks, h->two_ok ? 2LL * h->two.blocks : 0);
   for (const Slab& s : h->slabs) {
     IngestArgs ia{};
     ia.nrows = s.nrows;
@@ -654,8 +688,8 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   }
   h->partials_cap = (int)cap;
   CUDA_TRY(h, cudaMalloc(&h->partials, sizeof(RedPartial) * (size_t)cap));
-  CUDA_TRY(h, cudaMalloc(&h->counter, sizeof(unsigned int)));
-  CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, sizeof(unsigned int), h->stream));
+  CUDA_TRY(h, cudaMalloc(&h->counter, 2 * sizeof(unsigned int)));
+  CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, 2 * sizeof(unsigned int), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
   CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
   CUDA_TRY(h, cudaMalloc(&h->rec, sizeof(double) * kRecN));
@@ -895,6 +929,25 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       left -= k;
     }
     return SW2D_OK;
+  }
+  if (h->two_ok) {  // two steps per launch; an odd step falls through below
+    while (nsteps >= 2) {
+      double* rec1 = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
+      double* rec2 =
+          h->red_level ? h->hist + (size_t)((h->steps + 1) % h->hist_len) * kRecN : h->rec;
+      StepArgs a = step_args(h, h->two, rec1);
+      a.red.expected = h->two.blocks;
+      a.red2 = a.red;
+      a.red2.partials = h->partials + h->two.blocks;
+      a.red2.counter = h->counter + 1;
+      a.red2.rec = rec2;
+      launch_step2(a, h->red_level, h->stream);
+      h->nlaunch++;
+      CUDA_TRY(h, cudaGetLastError());
+      h->cur = 1 - h->cur;
+      h->steps += 2;
+      nsteps -= 2;
+    }
   }
   const bool p2p = h->halo_mode == SW2D_HALO_P2P && (h->virt || h->multi);
   const auto& mo = sw2d_host::memops();

@@ -108,17 +108,23 @@ struct StepArgs {
   int nsegs;                 // warp segments down the rows
   Coef c;
   RedArgs red;
+  RedArgs red2;              // two-step launches: the second step's record
 };
 
 // Step-kernel launchers (sw2d_kernels.cu).  `red_level`: 0 none, 1 sums
 // (VOLUME, SUM_ETA), 2 all diagnostics.  `kind`: 0 = one warp per CTA with
 // its own TMA row ring; 1 = CTA of kCtaStrips compute warps + a producer warp
-// sharing one TMA row ring (default).
+// sharing one TMA row ring (default); 2 = small grids: 2 columns per lane,
+// plain loads, 4 independent warps per CTA.
 int step_strips_per_cta(int kind);
+int step_strip_cols(int kind);   // output columns per warp strip (120, or 60 for kind 2)
 int step_grid(int kind, int nstrips, int nsegs);   // CTAs of one step launch
 void launch_step(const StepArgs& a, int red_level, int kind, void* stream,
                  bool remote = false);
 int step_occupancy_blocks_per_sm(int red_level, int kind);
+// Two steps per launch (kind 1 layout, one slab): state n -> n+2.
+void launch_step2(const StepArgs& a, int red_level, void* stream);
+int step2_strips_per_cta();
 
 // set_state helper: checks finiteness of the interior, zeroes the wall faces
 // of U (k = nx) and V (global j = ny), and sums hzero in fp64 into *h0sum.

@@ -66,6 +66,7 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
   __shared__ Acc sh[NW];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();  // sh / last may still be read by a previous call
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
     acc.sum_eta += shfl_xor_d(acc.sum_eta, m);
@@ -103,51 +104,52 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
     last = (ticket == (unsigned)(r.expected - 1));
   }
   __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // Fixed-order fold: thread t takes slots t, t+128, ... in order, then a
-  // fixed tree over threads.
-  Acc t;
-  t.init();
-  for (int i = threadIdx.x; i < r.expected; i += 32 * NW) {
-    const volatile RedPartial* p = r.partials + i;
-    t.sum_eta += p->sum_eta;
-    t.wet += p->wet;
-    t.max_eta = fmaxf(t.max_eta, p->max_eta);
-    t.neg_min_eta = fmaxf(t.neg_min_eta, p->neg_min_eta);
-    t.max_u = fmaxf(t.max_u, p->max_u);
-    t.max_v = fmaxf(t.max_v, p->max_v);
-  }
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    t.sum_eta += shfl_xor_d(t.sum_eta, m);
-    t.wet += shfl_xor_d(t.wet, m);
-    t.max_eta = fmaxf(t.max_eta, __shfl_xor_sync(kFull, t.max_eta, m));
-    t.neg_min_eta = fmaxf(t.neg_min_eta, __shfl_xor_sync(kFull, t.neg_min_eta, m));
-    t.max_u = fmaxf(t.max_u, __shfl_xor_sync(kFull, t.max_u, m));
-    t.max_v = fmaxf(t.max_v, __shfl_xor_sync(kFull, t.max_v, m));
-  }
-  __syncthreads();
-  if (lane == 0) sh[warp] = t;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    Acc f = sh[0];
-    for (int w = 1; w < NW; ++w) {
-      f.sum_eta += sh[w].sum_eta;
-      f.wet += sh[w].wet;
-      f.max_eta = fmaxf(f.max_eta, sh[w].max_eta);
-      f.neg_min_eta = fmaxf(f.neg_min_eta, sh[w].neg_min_eta);
-      f.max_u = fmaxf(f.max_u, sh[w].max_u);
-      f.max_v = fmaxf(f.max_v, sh[w].max_v);
+  if (last) {  // block-uniform
+    __threadfence();
+    // Fixed-order fold: thread t takes slots t, t+32*NW, ... in order, then a
+    // fixed tree over threads.
+    Acc t;
+    t.init();
+    for (int i = threadIdx.x; i < r.expected; i += 32 * NW) {
+      const volatile RedPartial* p = r.partials + i;
+      t.sum_eta += p->sum_eta;
+      t.wet += p->wet;
+      t.max_eta = fmaxf(t.max_eta, p->max_eta);
+      t.neg_min_eta = fmaxf(t.neg_min_eta, p->neg_min_eta);
+      t.max_u = fmaxf(t.max_u, p->max_u);
+      t.max_v = fmaxf(t.max_v, p->max_v);
     }
-    r.rec[kRecVol] = r.dxdy * (*r.h0sum + f.sum_eta);
-    r.rec[kRecSumEta] = f.sum_eta;
-    r.rec[kRecWet] = f.wet;
-    r.rec[kRecMaxEta] = f.max_eta;
-    r.rec[kRecNegMinEta] = f.neg_min_eta;
-    r.rec[kRecMaxU] = f.max_u;
-    r.rec[kRecMaxV] = f.max_v;
-    *r.counter = 0u;  // ready for the next step (stream-ordered)
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      t.sum_eta += shfl_xor_d(t.sum_eta, m);
+      t.wet += shfl_xor_d(t.wet, m);
+      t.max_eta = fmaxf(t.max_eta, __shfl_xor_sync(kFull, t.max_eta, m));
+      t.neg_min_eta = fmaxf(t.neg_min_eta, __shfl_xor_sync(kFull, t.neg_min_eta, m));
+      t.max_u = fmaxf(t.max_u, __shfl_xor_sync(kFull, t.max_u, m));
+      t.max_v = fmaxf(t.max_v, __shfl_xor_sync(kFull, t.max_v, m));
+    }
+    __syncthreads();
+    if (lane == 0) sh[warp] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Acc f = sh[0];
+      for (int w = 1; w < NW; ++w) {
+        f.sum_eta += sh[w].sum_eta;
+        f.wet += sh[w].wet;
+        f.max_eta = fmaxf(f.max_eta, sh[w].max_eta);
+        f.neg_min_eta = fmaxf(f.neg_min_eta, sh[w].neg_min_eta);
+        f.max_u = fmaxf(f.max_u, sh[w].max_u);
+        f.max_v = fmaxf(f.max_v, sh[w].max_v);
+      }
+      r.rec[kRecVol] = r.dxdy * (*r.h0sum + f.sum_eta);
+      r.rec[kRecSumEta] = f.sum_eta;
+      r.rec[kRecWet] = f.wet;
+      r.rec[kRecMaxEta] = f.max_eta;
+      r.rec[kRecNegMinEta] = f.neg_min_eta;
+      r.rec[kRecMaxU] = f.max_u;
+      r.rec[kRecMaxV] = f.max_v;
+      *r.counter = 0u;  // ready for the next step (stream-ordered)
+    }
   }
 }
 
@@ -164,22 +166,34 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
 // (fadd is commutative), so the window is two rows deep everywhere.
 // ---------------------------------------------------------------------------
 
-// rolling window carried from row L-1 into row L
-struct Win {
-  float e[4];      // eta(L-1)
-  float h[4];      // h(L-1)
-  float un[4];     // un(L-1)
-  float v[4];      // V(L-1), old
-  float fy[4];     // y-flux through the north face of row L-2
-  float A[4];      // Shapiro of row L-2: t1 + t2
-  float sS[4];     // Shapiro of row L-2: sel(wS, etan(L-3))
-  float etC[4];    // etan(L-2)
-  float h0P[4];    // hzero(L-1)   (diagnostics level 2)
-  float h0PP[4];   // hzero(L-2)   (diagnostics level 2)
-  float hR;        // h(L-1, k0+4)
-  unsigned wext;   // wet bits of row L-1: bit c+1 = column k0+c, c = -1..4
+// rolling window carried from row L-1 into row L (C columns per lane)
+template <int C>
+struct WinT {
+  float e[C];      // eta(L-1)
+  float h[C];      // h(L-1)
+  float un[C];     // un(L-1)
+  float v[C];      // V(L-1), old
+  float fy[C];     // y-flux through the north face of row L-2
+  float A[C];      // Shapiro of row L-2: t1 + t2
+  float sS[C];     // Shapiro of row L-2: sel(wS, etan(L-3))
+  float etC[C];    // etan(L-2)
+  float h0P[C];    // hzero(L-1)   (diagnostics level 2)
+  float h0PP[C];   // hzero(L-2)   (diagnostics level 2)
+  float hR;        // h(L-1, k0+C)
+  unsigned wext;   // wet bits of row L-1: bit c+1 = column k0+c, c = -1..C
   unsigned wPP;    // wet bits of row L-2: bit c = column k0+c
+  __device__ void zero() {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      e[c] = h[c] = un[c] = v[c] = fy[c] = 0.0f;
+      A[c] = sS[c] = etC[c] = h0P[c] = h0PP[c] = 0.0f;
+    }
+    hR = 0.0f;
+    wext = 0;
+    wPP = 0;
+  }
 };
+using Win = WinT<4>;
 
 struct Ctx {
   float cgx, cgy, cx, cy, q, hmin;
@@ -199,6 +213,7 @@ struct Ctx {
 };
 
 // P2P halo: mirror an output row into the neighbour slabs that need it
+// (the CTA kernel, 4 columns per lane)
 __device__ __forceinline__ void remote_store(const Ctx& x, int field, int row, float a, float b,
                                              float c, float d) {
 #pragma unroll
@@ -239,22 +254,42 @@ __device__ __forceinline__ float face(bool wc, bool wn, float d, float old) {
 }
 
 // One loaded row L: reads the window `w` (rows L-1, L-2), writes `o`.
-template <int RED, bool REMOTE>
-__device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
-                                         const float4 H4, const float4 U4,
-                                         const float4 V4, const int L, const Ctx& x,
-                                         Acc& acc, float* pU, float* pV, float* pE) {
-  const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
-  const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
-  const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
-  const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+// C consecutive floats of a row (C = 4: float4, C = 2: float2)
+template <int C>
+__device__ __forceinline__ void stC(float* p, const float (&v)[C]) {
+  if constexpr (C == 4) {
+    st4(p, v[0], v[1], v[2], v[3]);
+  } else if constexpr (C == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c) p[c] = v[c];
+  }
+}
+
+// the new-state values one row_stepC produces: u'(L), v'(L-1), eta'(L-2)
+template <int C>
+struct RowOut {
+  float un[C], vn[C], En[C];
+};
+
+// STORE: write the outputs of this segment's rows to global memory; else
+// return them in `out` (the first step of a two-step pass keeps its state in
+// registers).  The diagnostics of the segment's rows are accumulated either way.
+template <int RED, bool REMOTE, int C, bool STORE = true>
+__device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const float (&eL)[C],
+                                         const float (&h0L)[C], const float (&uL)[C],
+                                         const float (&vL)[C], const int L, const Ctx& x,
+                                         Acc& acc, float* pU, float* pV, float* pE,
+                                         RowOut<C>* out = nullptr) {
+  constexpr unsigned kMask = (1u << C) - 1u;
 
   // a1: h and wet flags of row L (rows outside 1..ny and columns outside
   // 1..nx are dry)
-  float hL[4];
+  float hL[C];
   unsigned wL = 0;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < C; ++c) {
     hL[c] = __fadd_rn(h0L[c], eL[c]);
     wL |= (hL[c] < x.hmin) ? 0u : (1u << c);
   }
@@ -263,15 +298,15 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   const float hR = __shfl_down_sync(kFull, hL[0], 1);
   const unsigned wRb = __shfl_down_sync(kFull, wL, 1);
   const unsigned wLb = __shfl_up_sync(kFull, wL, 1);
-  const unsigned wext = ((wLb >> 3) & 1u) | (wL << 1) | ((wRb & 1u) << 5);
+  const unsigned wext = ((wLb >> (C - 1)) & 1u) | (wL << 1) | ((wRb & 1u) << (C + 1));
 
   // a2: un(L) on the east faces of row L; vn(L-1) on the north faces of L-1
-  const unsigned wP = (w.wext >> 1) & 15u;
+  const unsigned wP = (w.wext >> 1) & kMask;
   const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north wall
-  float un[4], vn[4];
+  float un[C], vn[C];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const float en = (c < 3) ? eL[c + 1] : eR;
+  for (int c = 0; c < C; ++c) {
+    const float en = (c < C - 1) ? eL[c + 1] : eR;
     const float du = __fmul_rn(x.cgx, __fsub_rn(en, eL[c]));
     const float u = face(bit(wext, c + 1), bit(wext, c + 2), du, uL[c]);
     un[c] = bit(x.umask, c) ? u : 0.0f;
@@ -281,38 +316,38 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   }
 
   // a3: fluxes of row L-1 and etan(L-1)
-  float fx[4], fy[4], et[4];
+  float fx[C], fy[C], et[C];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    fx[c] = flux(w.un[c], w.h[c], (c < 3) ? w.h[c + 1] : w.hR);
+  for (int c = 0; c < C; ++c) {
+    fx[c] = flux(w.un[c], w.h[c], (c < C - 1) ? w.h[c + 1] : w.hR);
     fy[c] = flux(vn[c], w.h[c], hL[c]);
   }
-  const float fxw = __shfl_up_sync(kFull, fx[3], 1);
+  const float fxw = __shfl_up_sync(kFull, fx[C - 1], 1);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < C; ++c) {
     const float fw = (c > 0) ? fx[c - 1] : fxw;
     et[c] = __fsub_rn(__fsub_rn(w.e[c], __fmul_rn(x.cx, __fsub_rn(fx[c], fw))),
                       __fmul_rn(x.cy, __fsub_rn(fy[c], w.fy[c])));
   }
 
   // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
-  float En[4];
+  float En[C];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < C; ++c) {
     const float t3 = __fmul_rn(x.q, __fadd_rn(bit(wP, c) ? et[c] : 0.0f, w.sS[c]));
     En[c] = bit(w.wPP, c) ? __fadd_rn(w.A[c], t3) : w.etC[c];
   }
 
   // a4 (first half) for row L-1: s, t1, t2, sS
-  const float etW = __shfl_up_sync(kFull, et[3], 1);
+  const float etW = __shfl_up_sync(kFull, et[C - 1], 1);
   const float etE = __shfl_down_sync(kFull, et[0], 1);
-  const unsigned cnt = spread4((w.wext >> 2) & 15u) + spread4(w.wext & 15u) +
+  const unsigned cnt = spread4((w.wext >> 2) & kMask) + spread4(w.wext & kMask) +
                        spread4(wL) + spread4(w.wPP);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < C; ++c) {
     const float s = (float)((cnt >> (8 * c)) & 0xffu);
     const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(x.q, s)), et[c]);
-    const float xE = bit(w.wext, c + 2) ? ((c < 3) ? et[c + 1] : etE) : 0.0f;
+    const float xE = bit(w.wext, c + 2) ? ((c < C - 1) ? et[c + 1] : etE) : 0.0f;
     const float xW = bit(w.wext, c) ? ((c > 0) ? et[c - 1] : etW) : 0.0f;
     o.A[c] = __fadd_rn(t1, __fmul_rn(x.q, __fadd_rn(xE, xW)));
     o.sS[c] = bit(w.wPP, c) ? w.etC[c] : 0.0f;
@@ -322,39 +357,44 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   if (x.out_lane) {
     if (in_rows(L, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
-      SW2D_CHECK(pU >= x.dU && pU + 4 <= x.dU + x.nelem);
+      if constexpr (STORE) SW2D_CHECK(pU >= x.dU && pU + C <= x.dU + x.nelem);
 #endif
-      st4(pU, un[0], un[1], un[2], un[3]);
-      if (REMOTE) remote_store(x, 1, L, un[0], un[1], un[2], un[3]);
+      if constexpr (STORE) stC<C>(pU, un);
+      if constexpr (REMOTE && C == 4) remote_store(x, 1, L, un[0], un[1], un[2], un[3]);
       if (RED >= 2) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(un[c]));
+        for (int c = 0; c < C; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(un[c]));
       }
     }
     if (in_rows(L - 1, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
-      SW2D_CHECK(pV >= x.dV && pV + 4 <= x.dV + x.nelem);
+      if constexpr (STORE) SW2D_CHECK(pV >= x.dV && pV + C <= x.dV + x.nelem);
 #endif
-      st4(pV, vn[0], vn[1], vn[2], vn[3]);
-      if (REMOTE) remote_store(x, 2, L - 1, vn[0], vn[1], vn[2], vn[3]);
+      if constexpr (STORE) stC<C>(pV, vn);
+      if constexpr (REMOTE && C == 4) remote_store(x, 2, L - 1, vn[0], vn[1], vn[2], vn[3]);
       if (RED >= 2) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vn[c]));
+        for (int c = 0; c < C; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vn[c]));
       }
     }
     if (in_rows(L - 2, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
-      SW2D_CHECK(pE >= x.dE && pE + 4 <= x.dE + x.nelem);
+      if constexpr (STORE) SW2D_CHECK(pE >= x.dE && pE + C <= x.dE + x.nelem);
 #endif
-      st4(pE, En[0], En[1], En[2], En[3]);
-      if (REMOTE) remote_store(x, 0, L - 2, En[0], En[1], En[2], En[3]);
+      if constexpr (STORE) stC<C>(pE, En);
+      if constexpr (REMOTE && C == 4) remote_store(x, 0, L - 2, En[0], En[1], En[2], En[3]);
       if (RED >= 1) {
         // columns outside 1..nx hold exactly 0 (their etan is 0)
-        acc.sum_eta += ((double)En[0] + (double)En[1]) + ((double)En[2] + (double)En[3]);
+        if constexpr (C == 4) {
+          acc.sum_eta += ((double)En[0] + (double)En[1]) + ((double)En[2] + (double)En[3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc.sum_eta += (double)En[c];
+        }
       }
       if (RED >= 2) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < C; ++c) {
           if (bit(x.colmask, c)) {
             acc.max_eta = fmaxf(acc.max_eta, En[c]);
             acc.neg_min_eta = fmaxf(acc.neg_min_eta, -En[c]);
@@ -365,9 +405,18 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
     }
   }
 
+  if constexpr (!STORE) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      out->un[c] = un[c];
+      out->vn[c] = vn[c];
+      out->En[c] = En[c];
+    }
+  }
+
   // the window for row L+1
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < C; ++c) {
     o.e[c] = eL[c];
     o.h[c] = hL[c];
     o.un[c] = un[c];
@@ -382,6 +431,19 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4,
   o.hR = hR;
   o.wPP = wP;
   o.wext = wext;
+}
+
+// float4 adapter (the TMA kernels: 4 columns per lane)
+template <int RED, bool REMOTE>
+__device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4, const float4 H4,
+                                         const float4 U4, const float4 V4, const int L,
+                                         const Ctx& x, Acc& acc, float* pU, float* pV,
+                                         float* pE) {
+  const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
+  const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
+  const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
+  const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+  row_stepC<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc, pU, pV, pE);
 }
 
 // --- TMA bulk-copy row ring (one per warp) ---------------------------------
@@ -503,14 +565,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
     __syncwarp();
 
     Win wa, wb;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      wa.e[c] = wa.h[c] = wa.un[c] = wa.v[c] = wa.fy[c] = 0.0f;
-      wa.A[c] = wa.sS[c] = wa.etC[c] = wa.h0P[c] = wa.h0PP[c] = 0.0f;
-    }
-    wa.hR = 0.0f;
-    wa.wext = 0;
-    wa.wPP = 0;
+    wa.zero();
 
     float* __restrict__ En = a.s.En;
     float* __restrict__ Un = a.s.Un;
@@ -684,14 +739,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     x.rem = a.rem;
 
     Win wa, wb;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      wa.e[c] = wa.h[c] = wa.un[c] = wa.v[c] = wa.fy[c] = 0.0f;
-      wa.A[c] = wa.sS[c] = wa.etC[c] = wa.h0P[c] = wa.h0PP[c] = 0.0f;
-    }
-    wa.hR = 0.0f;
-    wa.wext = 0;
-    wa.wPP = 0;
+    wa.zero();
 
     float* __restrict__ En = a.s.En;
     float* __restrict__ Un = a.s.Un;
@@ -737,6 +785,289 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
   } else if (kCtaBarrierAtExit) {
     __syncthreads();  // keep the producer warp resident until the compute warps finish
   }
+}
+
+// --- Two steps per pass (the CTA ring kernel, single slab) ------------------
+// A second row march, fed from registers, advances the first march's output
+// by one more step before anything is written: state n is read once and
+// state n+2 written once, 28 B per two cell-steps.  The second march runs two
+// rows behind the first (its input row m = L-2 needs eta(n+1) of row L-2,
+// which the first march completes when it loads row L), so a segment of R
+// output rows streams R + 8 input rows.  The 4-column halo lanes cover the two
+// steps' cone (2 columns each).  Both steps keep the oracle's arithmetic
+// (bitwise), and both steps' diagnostics are folded (two records).
+template <int C>
+struct Win2 {
+  WinT<C> s1, s2;          // the two marches' windows
+  float unB1[C], unB2[C];  // u(n+1) of rows L-1, L-2
+  float vnB1[C];           // v(n+1) of row L-2
+  float h0B1[C], h0B2[C];  // hzero of rows L-1, L-2
+  __device__ void zero() {
+    s1.zero();
+    s2.zero();
+#pragma unroll
+    for (int c = 0; c < C; ++c) unB1[c] = unB2[c] = vnB1[c] = h0B1[c] = h0B2[c] = 0.0f;
+  }
+};
+
+template <int RED>
+__device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const float4 E4,
+                                          const float4 H4, const float4 U4, const float4 V4,
+                                          const int L, const Ctx& x, Acc& acc1, Acc& acc2,
+                                          float* pU, float* pV, float* pE) {
+  const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
+  const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
+  const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
+  const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+  RowOut<4> r1;
+  row_stepC<RED, false, 4, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
+                                  nullptr, &r1);
+  // state n+1 of row L-2: eta from this iteration, u from two, v from one back
+  row_stepC<RED, false, 4, true>(w.s2, o.s2, r1.En, w.h0B2, w.unB2, w.vnB1, L - 2, x, acc2, pU,
+                                 pV, pE);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    o.unB2[c] = w.unB1[c];
+    o.unB1[c] = r1.un[c];
+    o.vnB1[c] = r1.vn[c];
+    o.h0B2[c] = w.h0B1[c];
+    o.h0B1[c] = h0L[c];
+  }
+}
+
+// 7 compute warps + the producer: 8 warps (2 per scheduler) can use up to 255
+// registers per thread; the two marches' windows need ~200.
+constexpr int kCta2Strips = 7;
+constexpr int kCta2Threads = 32 * (kCta2Strips + 1);
+constexpr int kCta2WinBytes = (kCta2Strips * kColsPerStrip + 8) * 4;
+constexpr int kCta2StageBytes = 4 * kCta2WinBytes;
+constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
+
+template <int RED>
+__global__ void __launch_bounds__(kCta2Threads, 1)
+    sw2d_step_cta2(const StepArgs a) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  unsigned char* ring = dsm;
+  const uint32_t sring = smem_u32(ring);
+  const uint32_t sfull = sring + kCtaStages * kCta2StageBytes;
+  const uint32_t sempty = sfull + 8 * kCtaStages;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
+  const int cc = blockIdx.x % ncc;
+  const int seg = blockIdx.x / ncc;
+  const int strip0 = (cc * a.nstrips) / ncc;
+  const int nact = ((cc + 1) * a.nstrips) / ncc - strip0;
+
+  Acc acc1, acc2;
+  acc1.init();
+  acc2.init();
+
+  const int ra = (int)a.row_lo + seg * a.rows_per_seg;
+  const int rb = min((int)a.row_hi, ra + a.rows_per_seg - 1);
+  const int first = ra - 4;          // first streamed row
+  const int n = rb + 4 - first + 1;  // rows streamed
+  const long long pitch = a.s.pitch;
+  const int srows = (int)(a.s.nelem / pitch);    // storage rows of each field
+  const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
+  const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < kCtaStages; ++st) {
+      mbar_init(sfull + 8 * st, 1);
+      mbar_init(sempty + 8 * st, nact);
+    }
+    fence_proxy_async();
+  }
+  __syncthreads();
+
+  if (warp == kCta2Strips) {
+    if (lane == 0) {
+      const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
+      for (int r = 0; r < n; ++r) {
+        const int st = r % kCtaStages;
+        if (r >= kCtaStages) {
+          const uint32_t ph = (uint32_t)(r / kCtaStages - 1) & 1u;
+          while (!mbar_try_wait(sempty + 8 * st, ph)) {
+          }
+        }
+        const uint32_t d = sring + st * kCta2StageBytes, b = sfull + 8 * st;
+        const int sr = sfirst + r;
+        if (sr < 0 || sr >= srows) {   // outside the stored rows: the consumers use zeros
+          mbar_expect_tx(b, 0);
+          continue;
+        }
+        const long long o = off0 + (long long)r * pitch;
+        SW2D_CHECK(o >= 0 && o + wb / 4 <= a.s.nelem);
+        mbar_expect_tx(b, 4u * wb);
+        bulk_g2s(d, a.s.E + o, wb, b);
+        bulk_g2s(d + kCta2WinBytes, a.s.H0 + o, wb, b);
+        bulk_g2s(d + 2 * kCta2WinBytes, a.s.U + o, wb, b);
+        bulk_g2s(d + 3 * kCta2WinBytes, a.s.V + o, wb, b);
+      }
+    }
+  } else if (warp < nact) {
+    Ctx x;
+    x.ra = ra;
+    x.rb = rb;
+    const int c0 = (strip0 + warp) * kColsPerStrip + kStripBase + lane * 4;
+    const int k0 = c0 - kColOff;
+    x.colmask = 0;
+    x.umask = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    x.q = a.c.q; x.hmin = a.c.hmin;
+    x.ny = (int)a.ny;
+    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+#ifdef SW2D_DEBUG_BOUNDS
+    x.dU = a.s.Un;
+    x.dV = a.s.Vn;
+    x.dE = a.s.En;
+    x.nelem = a.s.nelem;
+#endif
+    Win2<4> wa, wb;
+    wa.zero();
+    float* __restrict__ En = a.s.En;
+    float* __restrict__ Un = a.s.Un;
+    float* __restrict__ Vn = a.s.Vn;
+    const long long lo = off0 + warp * kColsPerStrip + lane * 4;
+    const int sl = (warp * kColsPerStrip + lane * 4) * 4;
+
+    auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
+      const int st = i % kCtaStages;
+      const uint32_t ph = (uint32_t)(i / kCtaStages) & 1u;
+      while (!mbar_try_wait(sfull + 8 * st, ph)) {
+      }
+      const int sr = sfirst + i;
+      if (sr < 0 || sr >= srows) {
+        E4 = H4 = U4 = V4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      } else {
+        const unsigned char* base = ring + st * kCta2StageBytes + sl;
+        E4 = *reinterpret_cast<const float4*>(base);
+        H4 = *reinterpret_cast<const float4*>(base + kCta2WinBytes);
+        U4 = *reinterpret_cast<const float4*>(base + 2 * kCta2WinBytes);
+        V4 = *reinterpret_cast<const float4*>(base + 3 * kCta2WinBytes);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + 8 * st);
+    };
+    // the second march's rows L-2, L-3, L-4 (output pointers)
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
+      fetch(i, E4, H4, U4, V4);
+      row_step2<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch);
+      fetch(i + 1, E4, H4, U4, V4);
+      row_step2<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
+                     Vn + o, En + o - pitch);
+    }
+    if (i < n) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 2) * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step2<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch);
+    }
+  }
+  if (RED >= 1) {
+    block_reduce_and_finalize<RED, kCta2Strips + 1>(acc1, a.red);
+    block_reduce_and_finalize<RED, kCta2Strips + 1>(acc2, a.red2);
+  } else {
+    __syncthreads();
+  }
+}
+
+// --- Small grids: C = 2 columns per lane, plain loads (kind 2) --------------
+// The paper's own grids (500^2 .. 2000^2) are L2-resident and latency-bound:
+// a warp's row march costs about one dependent chain per row.  This variant
+// halves the columns per lane (60 output columns per warp strip), doubling
+// the warps that march in parallel, and loads rows with plain 64-bit loads
+// (one row prefetched in registers) instead of a TMA ring whose start-up
+// latency would not be amortised over a few rows.
+constexpr int kSmallC = 2;
+constexpr int kSmallWarps = 4;
+constexpr int kSmallCols = kOutLanes * kSmallC;   // 60 output columns per strip
+
+__device__ __forceinline__ void ldg2(const float* p, float (&v)[2]) {
+  const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+  v[0] = t.x;
+  v[1] = t.y;
+}
+
+template <int RED>
+__global__ void __launch_bounds__(32 * kSmallWarps)
+    sw2d_step_small(const StepArgs a) {
+  constexpr int C = kSmallC;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kSmallWarps + (threadIdx.x >> 5);
+  const int strip = gw % a.nstrips;
+  const int seg = gw / a.nstrips;
+  Acc acc;
+  acc.init();
+  if (seg < a.nsegs) {  // warp-uniform
+    Ctx x;
+    x.ra = (int)a.row_lo + seg * a.rows_per_seg;
+    x.rb = min((int)a.row_hi, x.ra + a.rows_per_seg - 1);
+    const int k0 = strip * kSmallCols + C * (lane - 1) + 1;  // 1-based column of element 0
+    const int c0 = k0 + kColOff;                              // its storage column
+    x.colmask = 0;
+    x.umask = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    x.q = a.c.q; x.hmin = a.c.hmin;
+    x.ny = (int)a.ny;
+    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+#ifdef SW2D_DEBUG_BOUNDS
+    x.dU = a.s.Un;
+    x.dV = a.s.Vn;
+    x.dE = a.s.En;
+    x.nelem = a.s.nelem;
+#endif
+    const long long pitch = a.s.pitch;
+    const int first = x.ra - 2, n = x.rb + 2 - first + 1;
+    const long long lo = (long long)(first - (int)a.s.jbase) * pitch + c0;
+    const float* __restrict__ E = a.s.E;
+    const float* __restrict__ H = a.s.H0;
+    const float* __restrict__ U = a.s.U;
+    const float* __restrict__ V = a.s.V;
+    float* __restrict__ En = a.s.En;
+    float* __restrict__ Un = a.s.Un;
+    float* __restrict__ Vn = a.s.Vn;
+    WinT<C> wa, wb;
+    wa.zero();
+    float aE[C], aH[C], aU[C], aV[C], bE[C], bH[C], bU[C], bV[C];
+    ldg2(E + lo, aE); ldg2(H + lo, aH); ldg2(U + lo, aU); ldg2(V + lo, aV);
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+      const long long o = lo + (long long)i * pitch, o1 = o + pitch;
+      ldg2(E + o1, bE); ldg2(H + o1, bH); ldg2(U + o1, bU); ldg2(V + o1, bV);
+      row_stepC<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc, Un + o,
+                               Vn + o - pitch, En + o - 2 * pitch);
+      if (i + 2 < n) {
+        const long long o2 = o1 + pitch;
+        ldg2(E + o2, aE); ldg2(H + o2, aH); ldg2(U + o2, aU); ldg2(V + o2, aV);
+      }
+      row_stepC<RED, false, C>(wb, wa, bE, bH, bU, bV, first + i + 1, x, acc, Un + o1, Vn + o,
+                               En + o - pitch);
+    }
+    if (i < n) {
+      const long long o = lo + (long long)i * pitch;
+      row_stepC<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc, Un + o,
+                               Vn + o - pitch, En + o - 2 * pitch);
+    }
+  }
+  if (RED >= 1) block_reduce_and_finalize<RED, kSmallWarps>(acc, a.red);
 }
 
 // ---------------------------------------------------------------------------
@@ -811,9 +1142,17 @@ int grid_stride_blocks(long long n) {
 
 }  // namespace
 
-int step_strips_per_cta(int kind) { return kind == 1 ? kCtaStrips : kStepWarps; }
+int step_strips_per_cta(int kind) {
+  return kind == 1 ? kCtaStrips : (kind == 2 ? kSmallWarps : kStepWarps);
+}
+
+int step_strip_cols(int kind) { return kind == 2 ? kSmallCols : kColsPerStrip; }
 
 int step_grid(int kind, int nstrips, int nsegs) {
+  if (kind == 2) {  // independent warps: (strip, segment) pairs, kSmallWarps per CTA
+    const long long warps = (long long)nstrips * nsegs;
+    return (int)((warps + kSmallWarps - 1) / kSmallWarps);
+  }
   const int per = step_strips_per_cta(kind);
   return ((nstrips + per - 1) / per) * nsegs;
 }
@@ -830,6 +1169,10 @@ void cta_attributes() {
 template <int RED, bool REMOTE>
 void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
   const int blocks = step_grid(kind, a.nstrips, a.nsegs);
+  if (kind == 2 && !REMOTE) {
+    sw2d_step_small<RED><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+    return;
+  }
   if (kind == 1 || REMOTE) {
     static unsigned long long attr_devices = 0;  // dynamic smem above 48 KB, per device
     int dev = 0;
@@ -847,7 +1190,9 @@ void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
 template <int RED>
 int occupancy_kind(int kind) {
   int n = 0;
-  if (kind == 1) {
+  if (kind == 2) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small<RED>, 32 * kSmallWarps, 0);
+  } else if (kind == 1) {
     cta_attributes<RED, false>();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED, false>, kCtaThreads,
                                                   kCtaSmem);
@@ -857,6 +1202,36 @@ int occupancy_kind(int kind) {
   return n < 1 ? 1 : n;
 }
 }  // namespace
+
+namespace {
+template <int RED>
+void launch_two(const StepArgs& a, cudaStream_t s) {
+  static unsigned long long attr_devices = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_devices >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(sw2d_step_cta2<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kCta2Smem);
+    cudaFuncSetAttribute(sw2d_step_cta2<RED>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         100);
+    attr_devices |= 1ull << (dev & 63);
+  }
+  const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
+  sw2d_step_cta2<RED><<<ncc * a.nsegs, kCta2Threads, kCta2Smem, s>>>(a);
+}
+}  // namespace
+
+int step2_strips_per_cta() { return kCta2Strips; }
+
+void launch_step2(const StepArgs& a, int red_level, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (red_level >= 2)
+    launch_two<2>(a, s);
+  else if (red_level == 1)
+    launch_two<1>(a, s);
+  else
+    launch_two<0>(a, s);
+}
 
 void launch_step(const StepArgs& a, int red_level, int kind, void* stream, bool remote) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -426,3 +426,31 @@ def test_snapshots_equal_oracle_states(dist):
         np.testing.assert_array_equal(out[k].numpy(), e)
     e, u, v = oracle.run(P, cur[0], cur[1], cur[2], cur[3], nsteps - nsnap * every)
     assert_state_equal(final[:3] + (None,), (e, u, v, None), where="after snapshots")
+
+
+# --- kernel variants forced on oracle-sized grids --------------------------
+
+@pytest.mark.parametrize("kind,two", [("1", "1"), ("1", "0"), ("0", "0"), ("2", "0")])
+@pytest.mark.parametrize("nx,ny,n", [(517, 389, 41), (241, 600, 30), (120, 121, 7), (9, 13, 5)])
+def test_kernel_kinds_bitwise(kind, two, nx, ny, n, monkeypatch):
+    """Every step-kernel kind on the same grids (the size heuristic picks
+    only one of them per grid): the CTA/TMA kernel with two steps per launch
+    (and an odd step count), one step per launch, the per-warp ring, and the
+    small-grid kernel — all bitwise equal to the oracle, with all fused
+    per-step diagnostics."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", kind)
+    monkeypatch.setenv("SW2D_TWO_STEP", two)
+    st = _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny)
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL)
+    assert_state_equal(got, want[:4], where=f"kind {kind} two {two} {nx}x{ny}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    for op, series in hist.items():
+        for k in range(n):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[k]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want[4][k, op]
+            check_reductions(row, ref)
+    got2, _, _, _ = gpu_run(P, st, n, chunks=[1, n - 1])
+    assert_state_equal(got2, want[:4], where=f"kind {kind} two {two} chunked")
