@@ -79,15 +79,35 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
-    """dram bytes per launch of the step kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def _ncu_summary():
     try:
-        with open(p) as f:
-            d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
     except Exception:
-        return None
+        return {}
+
+
+def ncu_traffic(workload, kernel):
+    """DRAM bytes per launch of `kernel` on `workload` from the committed ncu
+    capture (profiles/ncu_summary.json), or None."""
+    d = _ncu_summary().get(workload, {}).get(kernel, {})
+    return d.get("dram_bytes_per_launch")
+
+
+def ncu_instr_per_cell_step(kernel):
+    for w in _ncu_summary().values():
+        d = w.get(kernel, {})
+        if "thread_instr_per_cell_step" in d:
+            return d["thread_instr_per_cell_step"]
+    return None
+
+
+def max_sm_mhz():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0
 
 
 class Clocks:
@@ -290,24 +310,42 @@ def run_ours(args, cfg, ws, rank, local):
         launches = sw2d.sw2d_launch_count(h) - l0
         value = nx * ny * T * args.steps / (ms * 1e-3)
 
-        # roofline of the step kernel (1 launch per model step at N=1; at N>1
-        # interior + boundary launches per step, timed together)
-        step_launches_per_model_step = launches / (T * args.steps)
-        t_step_s = ms * 1e-3 / (T * args.steps)
+        # roofline of the step kernel.  One launch advances `spl` model steps
+        # (2: the two-step kernel on one slab; 1: one step; at N>1 interior +
+        # boundary launches per step are timed together).
+        red_lvl = 0 if not mask else (1 if mask < 4 else 2)
+        launches_per_step = launches / (T * args.steps)
+        spl = 2 if (args.variant == "fused" and launches_per_step < 0.75) else 1
+        t_launch_s = ms * 1e-3 / (T * args.steps) * spl
         cells_local = nrows * nx
         bpc = BYTES_PER_CELL if args.variant == "fused" else PAPER_BYTES_PER_CELL
-        achieved = bpc * cells_local / t_step_s / 1e9
+        alg_bytes = bpc * cells_local            # state in + state out, per launch
+        hbm_achieved = alg_bytes / t_launch_s / 1e9
         peak, peak_src = hbm_peak()
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(cfg["name"]) if args.variant == "fused" else None,
-                "algorithmic_bytes_per_launch": bpc * cells_local,
-                "kernel": ("sw2d_step_cta<%d>" % (0 if not mask else (1 if mask < 4 else 2)))
-                if args.variant == "fused" else
-                "paper_momentum + paper_continuity + paper_shapiro_update (per step)",
-                "launches_per_model_step": step_launches_per_model_step,
-                "peak_source": peak_src,
-                "note": "per-model-step time of the whole timed region (the step kernel "
-                        "is the only kernel per step; its fused last-CTA fold included)"}
+        kname = ("sw2d_step_cta2<%d>" if spl == 2 else "sw2d_step_cta<%d, 0>") % red_lvl
+        if args.variant != "fused":
+            kname = "paper_momentum + paper_continuity + paper_shapiro_update (per step)"
+        hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s",
+               "frac": hbm_achieved / peak, "peak_source": peak_src,
+               "traffic": ncu_traffic(cfg["name"], kname) if args.variant == "fused" else None,
+               "algorithmic_bytes_per_launch": alg_bytes, "model_steps_per_launch": spl}
+        roof = dict(hbm, kernel=kname, launches_per_model_step=launches_per_step)
+        ipc = ncu_instr_per_cell_step(kname)
+        if spl == 2 and ipc:
+            # two steps per launch move 14 B per cell-step: the launch is bound by
+            # instruction issue: 4 warp-instr/clk/SM x 32
+            # lanes x SMs x max SM clock
+            sm_hz = max_sm_mhz() * 1e6
+            sms = torch.cuda.get_device_properties(local).multi_processor_count
+            issue_peak = 4 * 32 * sms * sm_hz / 1e12
+            ach = ipc * (cells_local * spl / t_launch_s) / 1e12
+            roof = {"bound": "alu", "achieved": ach, "peak": issue_peak, "unit": "Tinstr/s",
+                    "frac": ach / issue_peak, "traffic": hbm["traffic"], "kernel": kname,
+                    "thread_instr_per_cell_step": ipc,
+                    "peak_source": "4 warp-instructions/clk/SM x 32 x %d SMs x %.0f MHz "
+                                   "(B200_PROFILING.md / B300_MICROARCH.md issue model)"
+                                   % (sms, sm_hz / 1e6),
+                    "launches_per_model_step": launches_per_step, "hbm_view": hbm}
 
         # --- periodic output overlapped with compute (optional) ------------
         snaps = None
