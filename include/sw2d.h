@@ -46,13 +46,16 @@
 extern "C" {
 #endif
 
-#define SW2D_ABI_VERSION 2
+#define SW2D_ABI_VERSION 3
+
+/* Halo depth (rows) of a row slab: the dependency cone of a two-step pass. */
+#define SW2D_HALO_ROWS 4
 
 typedef struct sw2d sw2d; /* opaque, library-owned */
 
 enum {
   SW2D_OK = 0,
-  SW2D_EINVAL = -1,      /* bad parameter, non-finite input, nrows < 4 per rank */
+  SW2D_EINVAL = -1,      /* bad parameter, non-finite input, nrows < 8 per rank */
   SW2D_ENOMEM = -2,      /* device allocation failed                           */
   SW2D_ECUDA = -3,       /* CUDA error (sticky)                                */
   SW2D_ENCCL = -4,       /* NCCL error or NCCL unavailable (sticky)            */
@@ -108,7 +111,7 @@ enum {
 };
 
 typedef struct {
-  int32_t rank, nranks;  /* row slabs along y (balanced); nrows >= 4 per rank     */
+  int32_t rank, nranks;  /* row slabs along y (balanced); nrows >= 8 per rank     */
   int32_t device;        /* CUDA ordinal for this rank (-1: current device)       */
   int32_t virtual_ranks; /* 1: run all nranks slabs in this one handle on one
                             device, halos copied device-to-device (no NCCL); the
@@ -123,15 +126,17 @@ int sw2d_abi_version(void);
 
 /* Pure host: rows [*j0, *j0 + *nrows) (0-based) of rank `rank` among `nranks`
  * balanced row slabs of a grid with ny rows.  SW2D_EINVAL if nranks < 1, rank
- * out of range, or a slab would have fewer than 4 rows (nranks > 1). */
+ * out of range, or a slab would have fewer than 2 * SW2D_HALO_ROWS = 8 rows
+ * (nranks > 1). */
 int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
                    int64_t* nrows);
 
-/* Pure host: the per-step halo exchange of rank `rank` among `nranks` row
- * slabs (the fused step's dependency cone is 2 rows: DESIGN.md "Multi-GPU").
- * A slab's fields are (nrows + 4)-row arrays: storage rows 0,1 are the south
- * halo, 2 .. nrows+1 the owned rows, nrows+2, nrows+3 the north halo.  Each
- * message is 2 consecutive storage rows of eta, u and v (of hzero once, in
+/* Pure host: the halo exchange of rank `rank` among `nranks` row slabs, done
+ * before every pass of one or two steps (the dependency cone of two steps is
+ * SW2D_HALO_ROWS = 4 rows: DESIGN.md "Multi-GPU").  A slab's fields are
+ * (nrows + 8)-row arrays: storage rows 0..3 are the south halo, 4 .. nrows+3
+ * the owned rows, nrows+4 .. nrows+7 the north halo.  Each message is
+ * SW2D_HALO_ROWS consecutive storage rows of eta, u and v (of hzero once, in
  * sw2d_set_state).  out[0] = first row sent to the south neighbour (rank-1),
  * out[1] = first row received from it, out[2] = first row sent to the north
  * neighbour (rank+1), out[3] = first row received from it; -1 where there is
@@ -146,7 +151,7 @@ int sw2d_nccl_unique_id(unsigned char out[128]);
 /* Create a handle.  dist == NULL: one GPU (the current device), whole grid.
  * cuda_stream: a cudaStream_t to enqueue on (e.g. torch's current stream), or
  * NULL for a library-owned stream.  Allocates 7 device arrays (hzero and
- * double-buffered eta, u, v) of (nrows + 4) x pitch floats.  *out = NULL on
+ * double-buffered eta, u, v) of (nrows + 8) x pitch floats.  *out = NULL on
  * failure. */
 int sw2d_create(const sw2d_params* params, const sw2d_dist* dist,
                 void* cuda_stream, sw2d** out);

@@ -26,7 +26,7 @@ namespace {
 
 thread_local std::string t_create_err;
 
-constexpr long long kSmallMaxCells = 1LL << 22;   // small-grid kernel up to 2048^2
+constexpr long long kSmallMaxCells = 1LL << 21;   // small-grid kernel up to ~1448^2
 constexpr int kMinRowsPerSeg = 4;   // small grids: more, shorter segments (latency-bound)
 constexpr int kDefaultHistory = 1024;
 
@@ -64,8 +64,8 @@ struct sw2d {
   std::vector<Slab> slabs;
   std::vector<Launch> launches;
   int step_blocks = 0;
-  Launch two{};          // two steps per launch (one slab): its single launch
-  bool two_ok = false;
+  std::vector<Launch> launches2;  // two steps per launch (kind 1): empty if unavailable
+  int step_blocks2 = 0;
   int cur = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -89,8 +89,7 @@ struct sw2d {
   int64_t steps = 0;
   int wcur = 0;  // paper variant: current wet buffer
   bool state_set = false;
-  bool pending_allreduce = false;
-  int64_t pending_step = 0;
+  std::vector<int64_t> pending;  // steps whose diagnostics await the allreduce (NCCL mode)
   int sticky = 0;
   std::string err;
   ncclComm_t comm_nccl = nullptr;
@@ -218,65 +217,59 @@ void plan_launches(sw2d* h) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
   int bps = step_occupancy_blocks_per_sm(h->red_level, h->kind);
   if (const char* e = std::getenv("SW2D_CTAS_PER_SM")) bps = std::max(1, std::min(bps, std::atoi(e)));
-  // one wave: resident CTAs / CTAs across the columns
-  const int per = step_strips_per_cta(h->kind);
-  const long long ncc = (h->nstrips + per - 1) / per;
-  const long long target_segs = std::max(1LL, (long long)sms * bps / ncc);
   long long min_rows = kMinRowsPerSeg;
   if (const char* e = std::getenv("SW2D_MIN_ROWS")) min_rows = std::max(1, std::atoi(e));
-  h->launches.clear();
-  int part = 0;
-  auto add = [&](int s, long long lo, long long hi, int phase) {
-    if (hi < lo) return;
-    const long long rows = hi - lo + 1;
-    long long rps = (rows + target_segs - 1) / target_segs;
-    rps = std::max<long long>(rps, min_rows);
-    Launch L;
-    L.slab = s;
-    L.row_lo = lo;
-    L.row_hi = hi;
-    L.rows_per_seg = (int)rps;
-    L.nsegs = (int)((rows + rps - 1) / rps);
-    L.phase = phase;
-    L.blocks = step_grid(h->kind, h->nstrips, L.nsegs);
-    L.part_base = part;
-    part += L.blocks;
-    h->launches.push_back(L);
+  // Rows within kHaloRows of an internal slab boundary read this step's
+  // halo (phase 1, after the exchange); the rest (phase 0) overlap with it.
+  // Virtual ranks use the same bands, so one GPU exercises the split.
+  auto plan = [&](std::vector<Launch>& out, int per, long long target_segs, long long mrows,
+                  int kind) {
+    out.clear();
+    int part = 0;
+    auto add = [&](int s, long long lo, long long hi, int phase) {
+      if (hi < lo) return;
+      const long long rows = hi - lo + 1;
+      long long rps = (rows + target_segs - 1) / target_segs;
+      rps = std::max<long long>(rps, mrows);
+      Launch L;
+      L.slab = s;
+      L.row_lo = lo;
+      L.row_hi = hi;
+      L.rows_per_seg = (int)rps;
+      L.nsegs = (int)((rows + rps - 1) / rps);
+      L.phase = phase;
+      L.blocks = kind == 3 ? (int)(((h->nstrips + per - 1) / per) * L.nsegs)
+                           : step_grid(kind, h->nstrips, L.nsegs);
+      L.part_base = part;
+      part += L.blocks;
+      out.push_back(L);
+    };
+    for (int s = 0; s < (int)h->slabs.size(); ++s) {
+      const Slab& sl = h->slabs[s];
+      const long long J0 = sl.j0 + 1, J1 = sl.j0 + sl.nrows;
+      const bool lo_halo = sl.j0 > 0, hi_halo = sl.j0 + sl.nrows < h->p.ny;
+      add(s, J0 + (lo_halo ? kHaloRows : 0), J1 - (hi_halo ? kHaloRows : 0), 0);
+      if (lo_halo) add(s, J0, J0 + kHaloRows - 1, 1);
+      if (hi_halo) add(s, J1 - kHaloRows + 1, J1, 1);
+    }
+    return part;
   };
-  for (int s = 0; s < (int)h->slabs.size(); ++s) {
-    const Slab& sl = h->slabs[s];
-    // rows within 2 of an internal slab boundary read this step's halo
-    // (phase 1, after the exchange); the rest (phase 0) overlap with it.
-    // Virtual ranks use the same bands, so one GPU exercises the split.
-    const long long J0 = sl.j0 + 1, J1 = sl.j0 + sl.nrows;
-    const bool lo_halo = sl.j0 > 0, hi_halo = sl.j0 + sl.nrows < h->p.ny;
-    add(s, J0 + (lo_halo ? 2 : 0), J1 - (hi_halo ? 2 : 0), 0);
-    if (lo_halo) add(s, J0, J0 + 1, 1);
-    if (hi_halo) add(s, J1 - 1, J1, 1);
+  {  // one step per launch
+    const int per = step_strips_per_cta(h->kind);
+    const long long ncc = (h->nstrips + per - 1) / per;
+    h->step_blocks = plan(h->launches, per, std::max(1LL, (long long)sms * bps / ncc), min_rows,
+                          h->kind);
   }
-  h->step_blocks = part;
-  plan_tb(h, sms);
-  // two steps per launch: one slab, the CTA kernel, no P2P halo
-  h->two_ok = false;
+  // two steps per launch (the CTA kernel layout; one CTA per SM)
+  h->launches2.clear();
+  h->step_blocks2 = 0;
   const char* two_env = std::getenv("SW2D_TWO_STEP");
-  if (!h->multi && !h->virt && h->kind == 1 && h->p.variant == SW2D_VARIANT_FUSED &&
-      h->halo_mode != SW2D_HALO_P2P && !(two_env && std::atoi(two_env) == 0)) {
+  if (h->kind == 1 && h->p.variant == SW2D_VARIANT_FUSED && !(two_env && std::atoi(two_env) == 0)) {
     const int per2 = step2_strips_per_cta();
     const long long ncc2 = (h->nstrips + per2 - 1) / per2;
-    const long long segs2 = std::max(1LL, (long long)sms / ncc2);
-    const long long rows = h->p.ny;
-    long long rps = std::max<long long>((rows + segs2 - 1) / segs2, 8);
-    Launch& L = h->two;
-    L.slab = 0;
-    L.row_lo = 1;
-    L.row_hi = rows;
-    L.rows_per_seg = (int)rps;
-    L.nsegs = (int)((rows + rps - 1) / rps);
-    L.blocks = (int)(ncc2 * L.nsegs);
-    L.part_base = 0;
-    L.phase = 0;
-    h->two_ok = true;
+    h->step_blocks2 = plan(h->launches2, per2, std::max(1LL, (long long)sms / ncc2), 8, 3);
   }
+  plan_tb(h, sms);
   if (std::getenv("SW2D_VERBOSE")) {
     if (h->tb_k)
       std::fprintf(stderr, "[sw2d] temporal blocking: %dx%d tiles, %d steps per launch\n",
@@ -286,9 +279,9 @@ void plan_launches(sw2d* h) {
     for (const Launch& L : h->launches)
       std::fprintf(stderr, "[sw2d]   slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
                    L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
-    if (h->two_ok)
-      std::fprintf(stderr, "[sw2d]   two steps per launch: %d segs x %d rows, %d CTAs\n",
-                   h->two.nsegs, h->two.rows_per_seg, h->two.blocks);
+    for (const Launch& L : h->launches2)
+      std::fprintf(stderr, "[sw2d]   2-step slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
+                   L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
   }
 }
 
@@ -356,8 +349,8 @@ void set_remotes(sw2d* h, const Launch& L, StepArgs& a) {
     a.rem[side].Vn = V;
     a.rem[side].jbase = jb;
     a.rem[side].nelem = ne;
-    a.rem[side].lo = (int)(side == 0 ? J0 : J1 - 1);
-    a.rem[side].hi = (int)(side == 0 ? J0 + 1 : J1);
+    a.rem[side].lo = (int)(side == 0 ? J0 : J1 - kHaloRows + 1);
+    a.rem[side].hi = (int)(side == 0 ? J0 + kHaloRows - 1 : J1);
   }
 }
 
@@ -624,13 +617,13 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     for (int r = 0; r < h->nranks; ++r) {
       Slab s;
       if (sw2d_partition(h->p.ny, h->nranks, r, &s.j0, &s.nrows) != SW2D_OK)
-        return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 4 rows per rank)");
+        return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 8 rows per rank)");
       h->slabs.push_back(s);
     }
   } else {
     Slab s;
     if (sw2d_partition(h->p.ny, h->nranks, h->rank, &s.j0, &s.nrows) != SW2D_OK)
-      return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 4 rows per rank)");
+      return fail(h, SW2D_EINVAL, "ny too small for nranks (need >= 8 rows per rank)");
     h->slabs.push_back(s);
   }
   // kernel kind: the CTA/TMA kernel, or the small-grid kernel for grids that
@@ -675,7 +668,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   }
   plan_launches(h);
   // reduction scratch
-  long long cap = std::max<long long>(h->step_blocks, h->two_ok ? 2LL * h->two.blocks : 0);
+  long long cap = std::max<long long>(h->step_blocks, 2LL * h->step_blocks2);
   for (const Slab& s : h->slabs) {
     IngestArgs ia{};
     ia.nrows = s.nrows;
@@ -692,7 +685,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, 2 * sizeof(unsigned int), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
   CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
-  CUDA_TRY(h, cudaMalloc(&h->rec, sizeof(double) * kRecN));
+  CUDA_TRY(h, cudaMalloc(&h->rec, 2 * sizeof(double) * kRecN));  // scratch: up to 2 steps
   CUDA_TRY(h, cudaMalloc(&h->h0sum, sizeof(double)));
   CUDA_TRY(h, cudaMalloc(&h->zero, sizeof(double)));
   CUDA_TRY(h, cudaMemsetAsync(h->zero, 0, sizeof(double), h->stream));
@@ -714,6 +707,101 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   return SW2D_OK;
 }
 
+// One pass of `spl` (1 or 2) model steps over every slab this handle holds:
+// the pass's halo exchange (device copies for virtual ranks, NCCL on the comm
+// stream, or in P2P mode a wait on the neighbours' flags), the interior
+// launches (phase 0, overlapping the exchange), the boundary launches
+// (phase 1; in P2P mode they also store their rows into the neighbours'
+// halos), the neighbours' signal, and the per-step diagnostics' allreduce.
+int run_pass(sw2d* h, int spl) {
+  const bool p2p = h->halo_mode == SW2D_HALO_P2P && (h->virt || h->multi);
+  const auto& mo = sw2d_host::memops();
+  const std::vector<Launch>& launches = spl == 2 ? h->launches2 : h->launches;
+  const int blocks = spl == 2 ? h->step_blocks2 : h->step_blocks;
+  double* rec[2];
+  for (int k = 0; k < 2; ++k)
+    rec[k] = h->red_level ? h->hist + (size_t)((h->steps + k) % h->hist_len) * kRecN
+                          : h->rec + k * kRecN;
+  if (h->virt && !p2p) {
+    int rc = virtual_halo(h, h->cur);
+    if (rc) return rc;
+  }
+  if (h->multi && !p2p) {
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+    int rc = nccl_halo(h, h->cur, h->comm);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+    for (int64_t st : h->pending) {  // the previous pass's diagnostics
+      rc = nccl_allreduce_rec(h, h->hist + (size_t)(st % h->hist_len) * kRecN, h->comm);
+      if (rc) return rc;
+    }
+    h->pending.clear();
+  }
+  auto args = [&](const Launch& L) {
+    StepArgs a = step_args(h, L, rec[0]);
+    a.red.expected = blocks;
+    a.red2 = a.red;
+    a.red2.partials = h->partials + blocks;
+    a.red2.counter = h->counter + 1;
+    a.red2.rec = rec[1];
+    return a;
+  };
+  auto launch = [&](const StepArgs& a, bool remote) {
+    if (spl == 2)
+      launch_step2(a, h->red_level, h->stream, remote);
+    else
+      launch_step(a, h->red_level, h->kind, h->stream, remote);
+    h->nlaunch++;
+  };
+  for (const Launch& L : launches)
+    if (L.phase == 0) launch(args(L), false);
+  bool any1 = false;
+  for (const Launch& L : launches) any1 |= L.phase == 1;
+  if (any1 && h->multi) {
+    if (p2p) {
+      const unsigned want = (unsigned)h->steps;  // neighbours have finished step want-1
+      for (int side = 0; side < 2; ++side)
+        if (h->nbr[side].present &&
+            mo.wait32(h->stream, (unsigned long long)(h->flags + side), want, 0x0 /*GEQ*/))
+          return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
+    } else {
+      CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    }
+  }
+  for (const Launch& L : launches)
+    if (L.phase == 1) {
+      StepArgs a = args(L);
+      if (p2p) set_remotes(h, L, a);
+      launch(a, p2p);
+    }
+  CUDA_TRY(h, cudaGetLastError());
+  if (h->multi) {
+    if (p2p) {  // tell the neighbours this pass's rows have landed in their halos
+      const unsigned done = (unsigned)(h->steps + spl);
+      for (int side = 0; side < 2; ++side)
+        if (h->nbr[side].present &&
+            mo.write32(h->stream, (unsigned long long)(h->nbr[side].flags + (1 - side)), done,
+                       0x0))
+          return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
+    }
+    CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
+    if (h->red_level) {
+      if (p2p) {
+        CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+        for (int k = 0; k < spl; ++k) {
+          int rc = nccl_allreduce_rec(h, rec[k], h->comm);
+          if (rc) return rc;
+        }
+      } else {
+        for (int k = 0; k < spl; ++k) h->pending.push_back(h->steps + k);
+      }
+    }
+  }
+  h->cur = 1 - h->cur;
+  h->steps += spl;
+  return SW2D_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -726,7 +814,7 @@ int sw2d_partition(int64_t ny, int32_t nranks, int32_t rank, int64_t* j0,
     return SW2D_EINVAL;
   const int64_t base = ny / nranks, rem = ny % nranks;
   const int64_t n = base + (rank < rem ? 1 : 0);
-  if (nranks > 1 && base < 4) return SW2D_EINVAL;  // the smallest slab
+  if (nranks > 1 && base < 2 * kHaloRows) return SW2D_EINVAL;  // the smallest slab
   *j0 = (int64_t)rank * base + std::min<int64_t>(rank, rem);
   *nrows = n;
   return SW2D_OK;
@@ -872,7 +960,7 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   h->cur = 0;
   h->steps = 0;
-  h->pending_allreduce = false;
+  h->pending.clear();
   h->state_set = false;
   if (bad) return fail(h, SW2D_EINVAL, "non-finite value in the input state");
   CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
@@ -930,103 +1018,19 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
     }
     return SW2D_OK;
   }
-  if (h->two_ok) {  // two steps per launch; an odd step falls through below
-    while (nsteps >= 2) {
-      double* rec1 = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
-      double* rec2 =
-          h->red_level ? h->hist + (size_t)((h->steps + 1) % h->hist_len) * kRecN : h->rec;
-      StepArgs a = step_args(h, h->two, rec1);
-      a.red.expected = h->two.blocks;
-      a.red2 = a.red;
-      a.red2.partials = h->partials + h->two.blocks;
-      a.red2.counter = h->counter + 1;
-      a.red2.rec = rec2;
-      launch_step2(a, h->red_level, h->stream);
-      h->nlaunch++;
-      CUDA_TRY(h, cudaGetLastError());
-      h->cur = 1 - h->cur;
-      h->steps += 2;
-      nsteps -= 2;
-    }
-  }
-  const bool p2p = h->halo_mode == SW2D_HALO_P2P && (h->virt || h->multi);
-  const auto& mo = sw2d_host::memops();
-  for (int64_t i = 0; i < nsteps; ++i) {
-    double* rec = h->red_level ? h->hist + (size_t)(h->steps % h->hist_len) * kRecN : h->rec;
-    if (h->virt && !p2p) {
-      int rc = virtual_halo(h, h->cur);
-      if (rc) return rc;
-    }
-    if (h->multi && !p2p) {
-      CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-      int rc = nccl_halo(h, h->cur, h->comm);
-      if (rc) return rc;
-      CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
-      if (h->pending_allreduce) {  // previous step's diagnostics
-        rc = nccl_allreduce_rec(h, h->hist + (size_t)(h->pending_step % h->hist_len) * kRecN,
-                                h->comm);
-        if (rc) return rc;
-        h->pending_allreduce = false;
-      }
-    }
-    // phase 0: rows that read no halo of this step (overlaps the exchange)
-    for (const Launch& L : h->launches)
-      if (L.phase == 0) {
-        launch_step(step_args(h, L, rec), h->red_level, h->kind, h->stream);
-        h->nlaunch++;
-      }
-    // phase 1: rows next to an internal boundary, after this step's halo
-    bool any1 = false;
-    for (const Launch& L : h->launches) any1 |= L.phase == 1;
-    if (any1 && h->multi) {
-      if (p2p) {
-        const unsigned want = (unsigned)h->steps;  // neighbours finished step want-1
-        for (int side = 0; side < 2; ++side)
-          if (h->nbr[side].present &&
-              mo.wait32(h->stream, (unsigned long long)(h->flags + side), want, 0x0 /*GEQ*/))
-            return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
-      } else {
-        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
-      }
-    }
-    for (const Launch& L : h->launches)
-      if (L.phase == 1) {
-        StepArgs a = step_args(h, L, rec);
-        if (p2p) set_remotes(h, L, a);
-        launch_step(a, h->red_level, h->kind, h->stream, p2p);
-        h->nlaunch++;
-      }
-    CUDA_TRY(h, cudaGetLastError());
-    if (h->multi) {
-      if (p2p) {  // tell the neighbours this step's rows have landed in their halos
-        const unsigned done = (unsigned)(h->steps + 1);
-        for (int side = 0; side < 2; ++side)
-          if (h->nbr[side].present &&
-              mo.write32(h->stream, (unsigned long long)(h->nbr[side].flags + (1 - side)), done,
-                         0x0))
-            return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
-      }
-      CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
-      if (h->red_level) {
-        if (p2p) {
-          CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-          int rc = nccl_allreduce_rec(h, rec, h->comm);
-          if (rc) return rc;
-        } else {
-          h->pending_allreduce = true;
-          h->pending_step = h->steps;
-        }
-      }
-    }
-    h->cur = 1 - h->cur;
-    h->steps++;
-  }
-  if (h->multi && h->pending_allreduce) {
-    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-    int rc = nccl_allreduce_rec(h, h->hist + (size_t)(h->pending_step % h->hist_len) * kRecN,
-                                h->comm);
+  while (nsteps > 0) {
+    const int spl = (nsteps >= 2 && !h->launches2.empty()) ? 2 : 1;
+    int rc = run_pass(h, spl);
     if (rc) return rc;
-    h->pending_allreduce = false;
+    nsteps -= spl;
+  }
+  if (h->multi && !h->pending.empty()) {
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+    for (int64_t st : h->pending) {
+      int rc = nccl_allreduce_rec(h, h->hist + (size_t)(st % h->hist_len) * kRecN, h->comm);
+      if (rc) return rc;
+    }
+    h->pending.clear();
   }
   if (h->multi && h->red_level) {
     // later work on the compute stream (reads of the history) follows the allreduces

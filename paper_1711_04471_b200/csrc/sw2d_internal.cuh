@@ -2,9 +2,9 @@
 // CUDA kernels (sw2d_kernels.cu) and the host runtime (sw2d_host.cu).
 //
 // Device layout: every field of a slab is a
-// row-major float32 array of (nrows + 4) rows x `pitch` floats.  Storage row
-// r holds global 1-based row j = jbase + r (jbase = first owned row - 2, so
-// two halo rows sit on each side).  Storage column c holds 1-based interior
+// row-major float32 array of (nrows + 8) rows x `pitch` floats.  Storage row
+// r holds global 1-based row j = jbase + r (jbase = first owned row - 4, so
+// four halo rows sit on each side: the dependency cone of a two-step pass).  Storage column c holds 1-based interior
 // column k = c - kColOff (k = 1 at c = 8; the west wall halo column k = 0 is
 // c = 7).  Warp strip s reads storage columns [120 s + 4, 120 s + 132) and
 // writes [120 s + 8, 120 s + 128): 15 whole 32-byte sectors, so no sector is
@@ -17,7 +17,7 @@ namespace sw2d_dev {
 
 constexpr int kColOff = 7;           // storage column of 1-based column k is k + 7
 constexpr int kStripBase = kColOff - 3;  // storage column where strip 0's window starts
-constexpr int kHaloRows = 2;         // halo rows per side (the fused step's cone)
+constexpr int kHaloRows = 4;         // halo rows per side: the cone of a two-step pass
 constexpr int kWarpsPerBlock = 4;      // grid-stride helper kernels
 constexpr int kThreads = 32 * kWarpsPerBlock;
 constexpr int kStepWarps = 1;          // step kernel: one warp per CTA (its strip
@@ -123,7 +123,7 @@ void launch_step(const StepArgs& a, int red_level, int kind, void* stream,
                  bool remote = false);
 int step_occupancy_blocks_per_sm(int red_level, int kind);
 // Two steps per launch (kind 1 layout, one slab): state n -> n+2.
-void launch_step2(const StepArgs& a, int red_level, void* stream);
+void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote = false);
 int step2_strips_per_cta();
 
 // set_state helper: checks finiteness of the interior, zeroes the wall faces

@@ -179,18 +179,19 @@ struct WinT {
   float etC[C];    // etan(L-2)
   float h0P[C];    // hzero(L-1)   (diagnostics level 2)
   float h0PP[C];   // hzero(L-2)   (diagnostics level 2)
+  float w1[C];     // wet flags (1.0 / 0.0) of row L-1
+  float w2[C];     // wet flags of row L-2
+  float w1W, w1E;  // wet flags of row L-1 at columns k0-1 and k0+C
   float hR;        // h(L-1, k0+C)
-  unsigned wext;   // wet bits of row L-1: bit c+1 = column k0+c, c = -1..C
-  unsigned wPP;    // wet bits of row L-2: bit c = column k0+c
   __device__ void zero() {
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       e[c] = h[c] = un[c] = v[c] = fy[c] = 0.0f;
       A[c] = sS[c] = etC[c] = h0P[c] = h0PP[c] = 0.0f;
+      w1[c] = w2[c] = 0.0f;
     }
+    w1W = w1E = 0.0f;
     hR = 0.0f;
-    wext = 0;
-    wPP = 0;
   }
 };
 using Win = WinT<4>;
@@ -199,6 +200,8 @@ struct Ctx {
   float cgx, cgy, cx, cy, q, hmin;
   unsigned colmask;  // columns 1..nx of this lane's four
   unsigned umask;    // columns 1..nx-1 (faces that are not the east wall)
+  float cmf[4];      // colmask as 1.0 / 0.0 per column
+  float umf[4];      // umask as 1.0 / 0.0 per column
   int ny, ra, rb;    // global rows (1-based): grid rows, this segment's output rows
   bool out_lane;
   int col;                 // storage column of this lane's element 0 (REMOTE only)
@@ -225,11 +228,6 @@ __device__ __forceinline__ void remote_store(const Ctx& x, int field, int row, f
       st4(base + (long long)(row - m.jbase) * x.pitch + x.col, a, b, c, d);
     }
   }
-}
-
-// the four byte-lanes of the result hold bits 0..3 of m (m < 16)
-__device__ __forceinline__ unsigned spread4(unsigned m) {
-  return (m * 0x00204081u) & 0x01010101u;
 }
 
 __device__ __forceinline__ bool bit(unsigned m, int i) { return (m >> i) & 1u; }
@@ -282,36 +280,36 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
                                          const float (&vL)[C], const int L, const Ctx& x,
                                          Acc& acc, float* pU, float* pV, float* pE,
                                          RowOut<C>* out = nullptr) {
-  constexpr unsigned kMask = (1u << C) - 1u;
+  // Wet flags are carried as 1.0f / 0.0f: a select sel(w, x) = w ? x : 0 is
+  // then the product w * x, equal in value for finite x (x * 0 is a zero of
+  // either sign; signed zeros never change a later non-zero value or a
+  // comparison here), and s = wE + wW + wN + wS is the exact integer count.
 
   // a1: h and wet flags of row L (rows outside 1..ny and columns outside
   // 1..nx are dry)
-  float hL[C];
-  unsigned wL = 0;
+  const bool rowok = in_rows(L, 1, x.ny);
+  float hL[C], wL[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     hL[c] = __fadd_rn(h0L[c], eL[c]);
-    wL |= (hL[c] < x.hmin) ? 0u : (1u << c);
+    wL[c] = (rowok && !(hL[c] < x.hmin)) ? x.cmf[c] : 0.0f;
   }
-  wL &= in_rows(L, 1, x.ny) ? x.colmask : 0u;
   const float eR = __shfl_down_sync(kFull, eL[0], 1);
   const float hR = __shfl_down_sync(kFull, hL[0], 1);
-  const unsigned wRb = __shfl_down_sync(kFull, wL, 1);
-  const unsigned wLb = __shfl_up_sync(kFull, wL, 1);
-  const unsigned wext = ((wLb >> (C - 1)) & 1u) | (wL << 1) | ((wRb & 1u) << (C + 1));
+  const float wR = __shfl_down_sync(kFull, wL[0], 1);
+  const float wLf = __shfl_up_sync(kFull, wL[C - 1], 1);
 
   // a2: un(L) on the east faces of row L; vn(L-1) on the north faces of L-1
-  const unsigned wP = (w.wext >> 1) & kMask;
   const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north wall
   float un[C], vn[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float en = (c < C - 1) ? eL[c + 1] : eR;
+    const float wn = (c < C - 1) ? wL[c + 1] : wR;
     const float du = __fmul_rn(x.cgx, __fsub_rn(en, eL[c]));
-    const float u = face(bit(wext, c + 1), bit(wext, c + 2), du, uL[c]);
-    un[c] = bit(x.umask, c) ? u : 0.0f;
+    un[c] = __fmul_rn(face(wL[c] != 0.0f, wn != 0.0f, du, uL[c]), x.umf[c]);
     const float dv = __fmul_rn(x.cgy, __fsub_rn(eL[c], w.e[c]));
-    const float v = face(bit(wP, c), bit(wL, c), dv, w.v[c]);
+    const float v = face(w.w1[c] != 0.0f, wL[c] != 0.0f, dv, w.v[c]);
     vn[c] = vrow ? v : 0.0f;
   }
 
@@ -334,23 +332,23 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float En[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const float t3 = __fmul_rn(x.q, __fadd_rn(bit(wP, c) ? et[c] : 0.0f, w.sS[c]));
-    En[c] = bit(w.wPP, c) ? __fadd_rn(w.A[c], t3) : w.etC[c];
+    const float t3 = __fmul_rn(x.q, __fadd_rn(__fmul_rn(w.w1[c], et[c]), w.sS[c]));
+    En[c] = (w.w2[c] != 0.0f) ? __fadd_rn(w.A[c], t3) : w.etC[c];
   }
 
   // a4 (first half) for row L-1: s, t1, t2, sS
   const float etW = __shfl_up_sync(kFull, et[C - 1], 1);
   const float etE = __shfl_down_sync(kFull, et[0], 1);
-  const unsigned cnt = spread4((w.wext >> 2) & kMask) + spread4(w.wext & kMask) +
-                       spread4(wL) + spread4(w.wPP);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const float s = (float)((cnt >> (8 * c)) & 0xffu);
+    const float wE = (c < C - 1) ? w.w1[c + 1] : w.w1E;
+    const float wW = (c > 0) ? w.w1[c - 1] : w.w1W;
+    const float s = __fadd_rn(__fadd_rn(__fadd_rn(wE, wW), wL[c]), w.w2[c]);
     const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(x.q, s)), et[c]);
-    const float xE = bit(w.wext, c + 2) ? ((c < C - 1) ? et[c + 1] : etE) : 0.0f;
-    const float xW = bit(w.wext, c) ? ((c > 0) ? et[c - 1] : etW) : 0.0f;
+    const float xE = __fmul_rn(wE, (c < C - 1) ? et[c + 1] : etE);
+    const float xW = __fmul_rn(wW, (c > 0) ? et[c - 1] : etW);
     o.A[c] = __fadd_rn(t1, __fmul_rn(x.q, __fadd_rn(xE, xW)));
-    o.sS[c] = bit(w.wPP, c) ? w.etC[c] : 0.0f;
+    o.sS[c] = __fmul_rn(w.w2[c], w.etC[c]);
   }
 
   // a5: commit (lanes 1..30, rows of this segment)
@@ -423,14 +421,16 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     o.v[c] = vL[c];
     o.fy[c] = fy[c];
     o.etC[c] = et[c];
+    o.w1[c] = wL[c];
+    o.w2[c] = w.w1[c];
     if (RED >= 2) {
       o.h0PP[c] = w.h0P[c];
       o.h0P[c] = h0L[c];
     }
   }
+  o.w1W = wLf;
+  o.w1E = wR;
   o.hR = hR;
-  o.wPP = wP;
-  o.wext = wext;
 }
 
 // float4 adapter (the TMA kernels: 4 columns per lane)
@@ -522,6 +522,11 @@ __global__ void __launch_bounds__(32 * kStepWarps)
     for (int c = 0; c < 4; ++c) {
       x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
       x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     x.q = a.c.q; x.hmin = a.c.hmin;
@@ -724,6 +729,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
       x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
+    }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
@@ -798,23 +808,23 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 // (bitwise), and both steps' diagnostics are folded (two records).
 template <int C>
 struct Win2 {
-  WinT<C> s1, s2;          // the two marches' windows
-  float unB1[C], unB2[C];  // u(n+1) of rows L-1, L-2
-  float vnB1[C];           // v(n+1) of row L-2
-  float h0B1[C], h0B2[C];  // hzero of rows L-1, L-2
+  WinT<C> s1, s2;  // the two marches' windows
   __device__ void zero() {
     s1.zero();
     s2.zero();
-#pragma unroll
-    for (int c = 0; c < C; ++c) unB1[c] = unB2[c] = vnB1[c] = h0B1[c] = h0B2[c] = 0.0f;
   }
 };
 
-template <int RED>
+// The state n+1 of row L-2 that the second march consumes is assembled from
+// slots updated in place (no shifting): uS / hS hold u(n+1) and hzero of the
+// row two iterations back (the caller alternates two slots), vS holds v(n+1)
+// of the row one iteration back.
+template <int RED, bool REMOTE>
 __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const float4 E4,
                                           const float4 H4, const float4 U4, const float4 V4,
                                           const int L, const Ctx& x, Acc& acc1, Acc& acc2,
-                                          float* pU, float* pV, float* pE) {
+                                          float* pU, float* pV, float* pE, float (&uS)[4],
+                                          float (&hS)[4], float (&vS)[4]) {
   const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
   const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
   const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
@@ -823,15 +833,12 @@ __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const fl
   row_stepC<RED, false, 4, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
                                   nullptr, &r1);
   // state n+1 of row L-2: eta from this iteration, u from two, v from one back
-  row_stepC<RED, false, 4, true>(w.s2, o.s2, r1.En, w.h0B2, w.unB2, w.vnB1, L - 2, x, acc2, pU,
-                                 pV, pE);
+  row_stepC<RED, REMOTE, 4, true>(w.s2, o.s2, r1.En, hS, uS, vS, L - 2, x, acc2, pU, pV, pE);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    o.unB2[c] = w.unB1[c];
-    o.unB1[c] = r1.un[c];
-    o.vnB1[c] = r1.vn[c];
-    o.h0B2[c] = w.h0B1[c];
-    o.h0B1[c] = h0L[c];
+    uS[c] = r1.un[c];
+    hS[c] = h0L[c];
+    vS[c] = r1.vn[c];
   }
 }
 
@@ -843,7 +850,7 @@ constexpr int kCta2WinBytes = (kCta2Strips * kColsPerStrip + 8) * 4;
 constexpr int kCta2StageBytes = 4 * kCta2WinBytes;
 constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
 
-template <int RED>
+template <int RED, bool REMOTE>
 __global__ void __launch_bounds__(kCta2Threads, 1)
     sw2d_step_cta2(const StepArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -920,10 +927,18 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
       x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
     }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
+    }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+    x.col = c0;
+    x.pitch = pitch;
+    x.rem = a.rem;
 #ifdef SW2D_DEBUG_BOUNDS
     x.dU = a.s.Un;
     x.dV = a.s.Vn;
@@ -932,6 +947,9 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
 #endif
     Win2<4> wa, wb;
     wa.zero();
+    float uA[4] = {0.f, 0.f, 0.f, 0.f}, uB[4] = {0.f, 0.f, 0.f, 0.f};
+    float hA[4] = {0.f, 0.f, 0.f, 0.f}, hB[4] = {0.f, 0.f, 0.f, 0.f};
+    float vS[4] = {0.f, 0.f, 0.f, 0.f};
     float* __restrict__ En = a.s.En;
     float* __restrict__ Un = a.s.Un;
     float* __restrict__ Vn = a.s.Vn;
@@ -962,18 +980,18 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
       fetch(i, E4, H4, U4, V4);
-      row_step2<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch);
+      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
       fetch(i + 1, E4, H4, U4, V4);
-      row_step2<RED>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
-                     Vn + o, En + o - pitch);
+      row_step2<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
+                     Vn + o, En + o - pitch, uB, hB, vS);
     }
     if (i < n) {
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)(i - 2) * pitch;
       fetch(i, E4, H4, U4, V4);
-      row_step2<RED>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch);
+      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
     }
   }
   if (RED >= 1) {
@@ -1023,6 +1041,11 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
     for (int c = 0; c < C; ++c) {
       x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
       x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     x.q = a.c.q; x.hmin = a.c.hmin;
@@ -1204,33 +1227,41 @@ int occupancy_kind(int kind) {
 }  // namespace
 
 namespace {
-template <int RED>
+template <int RED, bool REMOTE>
 void launch_two(const StepArgs& a, cudaStream_t s) {
   static unsigned long long attr_devices = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_devices >> (dev & 63) & 1ull)) {
-    cudaFuncSetAttribute(sw2d_step_cta2<RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kCta2Smem);
-    cudaFuncSetAttribute(sw2d_step_cta2<RED>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         100);
+    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kCta2Smem);
+    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     attr_devices |= 1ull << (dev & 63);
   }
   const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
-  sw2d_step_cta2<RED><<<ncc * a.nsegs, kCta2Threads, kCta2Smem, s>>>(a);
+  sw2d_step_cta2<RED, REMOTE><<<ncc * a.nsegs, kCta2Threads, kCta2Smem, s>>>(a);
 }
 }  // namespace
 
 int step2_strips_per_cta() { return kCta2Strips; }
 
-void launch_step2(const StepArgs& a, int red_level, void* stream) {
+void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (red_level >= 2)
-    launch_two<2>(a, s);
-  else if (red_level == 1)
-    launch_two<1>(a, s);
-  else
-    launch_two<0>(a, s);
+  if (remote) {
+    if (red_level >= 2)
+      launch_two<2, true>(a, s);
+    else if (red_level == 1)
+      launch_two<1, true>(a, s);
+    else
+      launch_two<0, true>(a, s);
+  } else if (red_level >= 2) {
+    launch_two<2, false>(a, s);
+  } else if (red_level == 1) {
+    launch_two<1, false>(a, s);
+  } else {
+    launch_two<0, false>(a, s);
+  }
 }
 
 void launch_step(const StepArgs& a, int red_level, int kind, void* stream, bool remote) {

@@ -45,7 +45,7 @@ def test_built_for_sm100a(lib):
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("ny,p", [(10, 1), (17, 2), (100, 3), (16384 * 8, 8), (9, 2)])
+@pytest.mark.parametrize("ny,p", [(10, 1), (17, 2), (100, 3), (16384 * 8, 8), (16, 2)])
 def test_partition_balanced_and_covering(lib, ny, p):
     rows = [sw2d.sw2d_partition(ny, p, r) for r in range(p)]
     assert rows[0][0] == 0
@@ -57,7 +57,7 @@ def test_partition_balanced_and_covering(lib, ny, p):
 
 
 def test_partition_rejects(lib):
-    for args in [(7, 2, 0), (10, 0, 0), (10, 2, 2), (10, 2, -1), (0, 1, 0)]:
+    for args in [(15, 2, 0), (10, 0, 0), (10, 2, 2), (10, 2, -1), (0, 1, 0)]:
         with pytest.raises(sw2d.Sw2dError) as ei:
             sw2d.sw2d_partition(*args)
         assert ei.value.code == sw2d.SW2D_EINVAL

@@ -195,7 +195,7 @@ def test_status_codes():
     finally:
         sw2d.sw2d_destroy(h)
     with pytest.raises(sw2d.Sw2dError) as ei:
-        sw2d.sw2d_create(sw2d.make_params(16, 7), sw2d.make_dist(0, 2, virtual_ranks=1))
+        sw2d.sw2d_create(sw2d.make_params(16, 15), sw2d.make_dist(0, 2, virtual_ranks=1))
     assert ei.value.code == sw2d.SW2D_EINVAL
 
 
@@ -454,3 +454,27 @@ def test_kernel_kinds_bitwise(kind, two, nx, ny, n, monkeypatch):
             check_reductions(row, ref)
     got2, _, _, _ = gpu_run(P, st, n, chunks=[1, n - 1])
     assert_state_equal(got2, want[:4], where=f"kind {kind} two {two} chunked")
+
+
+@pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
+@pytest.mark.parametrize("two", ["1", "0"])
+@pytest.mark.parametrize("nranks,n", [(2, 31), (3, 8), (5, 17)])
+def test_virtual_ranks_kinds_bitwise(nranks, n, two, halo, monkeypatch):
+    """Row slabs with the CTA kernel (forced), one or two steps per launch,
+    NCCL-plan device copies or fused P2P halo stores: bitwise equal to the
+    oracle, diagnostics folded over all slabs, odd step counts included."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", "1")
+    monkeypatch.setenv("SW2D_TWO_STEP", two)
+    cfg, st = _bowl(263, 97)
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL,
+                                dist=sw2d.make_dist(0, nranks, virtual_ranks=1, halo_mode=halo))
+    assert_state_equal(got, want[:4], where=f"{nranks} slabs two={two} halo={halo}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    for op, series in hist.items():
+        for k in range(n):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[k]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want[4][k, op]
+            check_reductions(row, ref)

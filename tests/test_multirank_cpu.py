@@ -37,22 +37,26 @@ def _cfg():
     return dict(si.config("c3"), nx=97, ny=61, sigma=4.0, seed=21)
 
 
+HALO = 4  # SW2D_HALO_ROWS (include/sw2d.h)
+
+
 def _exchange(arrs, plan, rank):
-    """Send/recv 2 storage rows per field with the neighbours (the plan)."""
+    """Send/recv HALO storage rows per field with the neighbours (the plan)."""
     reqs, landing = [], []
     for side, peer in ((0, rank - 1), (1, rank + 1)):
         snd, rcv = plan[2 * side], plan[2 * side + 1]
         if snd < 0:
             continue
         for a in arrs:
-            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(a[snd:snd + 2])), peer))
-            buf = torch.empty((2, a.shape[1]), dtype=torch.float32)
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(a[snd:snd + HALO])),
+                                   peer))
+            buf = torch.empty((HALO, a.shape[1]), dtype=torch.float32)
             reqs.append(dist.irecv(buf, peer))
             landing.append((a, rcv, buf))
     for r in reqs:
         r.wait()
     for a, rcv, buf in landing:
-        a[rcv:rcv + 2] = buf.numpy()
+        a[rcv:rcv + HALO] = buf.numpy()
 
 
 def _worker(rank, world, port, nsteps, result_path):
@@ -64,21 +68,22 @@ def _worker(rank, world, port, nsteps, result_path):
         ny, nx = cfg["ny"], cfg["nx"]
         j0, nrows = sw2d.sw2d_partition(ny, world, rank)
         plan = sw2d.sw2d_halo_plan(ny, world, rank)
-        # storage rows 0..nrows+3 <-> global rows j0-2 .. j0+nrows+1
-        st = [np.zeros((nrows + 4, nx), np.float32) for _ in range(4)]
+        # storage rows 0..nrows+2H-1 <-> global rows j0-H .. j0+nrows+H-1
+        st = [np.zeros((nrows + 2 * HALO, nx), np.float32) for _ in range(4)]
         own = si.generate(cfg, j0=j0, nrows=nrows)
         for a, o in zip(st, own):
-            a[2:nrows + 2] = o
+            a[HALO:nrows + HALO] = o
         hz, e, u, v = st
         _exchange([hz], plan, rank)                  # static hzero halo, once
-        s_lo = 0 if plan[1] >= 0 else 2              # window: storage rows in the grid
-        s_hi = nrows + 4 if plan[3] >= 0 else nrows + 2
+        s_lo = 0 if plan[1] >= 0 else HALO           # window: storage rows in the grid
+        s_hi = nrows + 2 * HALO if plan[3] >= 0 else nrows + HALO
         for _ in range(nsteps):
             _exchange([e, u, v], plan, rank)         # state-n halos
             w = oracle.run(P, hz[s_lo:s_hi], e[s_lo:s_hi], u[s_lo:s_hi], v[s_lo:s_hi], 1)
             for a, b in zip((e, u, v), w):
                 a[s_lo:s_hi] = b
-        owned = torch.from_numpy(np.stack([e[2:nrows + 2], u[2:nrows + 2], v[2:nrows + 2]]))
+        sl = slice(HALO, nrows + HALO)
+        owned = torch.from_numpy(np.stack([e[sl], u[sl], v[sl]]))
         sizes = [sw2d.sw2d_partition(ny, world, r)[1] for r in range(world)]
         if rank == 0:
             parts = [owned] + [torch.empty((3, n, nx), dtype=torch.float32) for n in sizes[1:]]
@@ -108,17 +113,17 @@ def test_slabs_with_halo_plan_equal_single_grid(world, tmp_path):
 
 def test_halo_plan_is_symmetric():
     """What a rank sends north is what its north neighbour receives from the
-    south, row counts 2, and the rows are owned rows / halo rows."""
+    south, and the rows are owned rows / halo rows."""
     for ny, world in [(16, 2), (61, 3), (1000, 8), (16384 * 8, 8)]:
         for r in range(world):
             j0, n = sw2d.sw2d_partition(ny, world, r)
             p = sw2d.sw2d_halo_plan(ny, world, r)
             if r > 0:
-                assert p[0] == 2 and p[1] == 0
+                assert p[0] == HALO and p[1] == 0
             else:
                 assert p[0] == p[1] == -1
             if r < world - 1:
-                assert p[2] == n and p[3] == n + 2
+                assert p[2] == n and p[3] == n + HALO
                 # the north neighbour's first owned storage row holds global row j0 + n
                 assert sw2d.sw2d_partition(ny, world, r + 1)[0] == j0 + n
             else:
