@@ -27,7 +27,13 @@ namespace {
 thread_local std::string t_create_err;
 
 constexpr long long kSmallMaxCells = 1LL << 21;   // small-grid kernel up to ~1448^2
-constexpr int kMinRowsPerSeg = 4;   // small grids: more, shorter segments (latency-bound)
+constexpr int kMinRowsPerSeg = 4;
+constexpr int kGraphPasses = 32;  // passes per captured CUDA graph (even)
+
+bool graphs_enabled() {
+  const char* e = std::getenv("SW2D_GRAPHS");
+  return !(e && std::atoi(e) == 0);
+}   // small grids: more, shorter segments (latency-bound)
 constexpr int kDefaultHistory = 1024;
 
 struct Slab {
@@ -90,6 +96,10 @@ struct sw2d {
   int wcur = 0;  // paper variant: current wet buffer
   bool state_set = false;
   std::vector<int64_t> pending;  // steps whose diagnostics await the allreduce (NCCL mode)
+  // CUDA graphs of kGraphPasses passes (one slab, no per-step diagnostics),
+  // one per starting buffer parity; replayed for long sw2d_step calls
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int graph_spl = 0;
   int sticky = 0;
   std::string err;
   ncclComm_t comm_nccl = nullptr;
@@ -538,6 +548,8 @@ void free_all(sw2d* h) {
     if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
   }
   cudaFree(h->flags);
+  for (int b = 0; b < 2; ++b)
+    if (h->graph[b]) cudaGraphExecDestroy(h->graph[b]);
   if (h->comm_nccl && sw2d_host::nccl().ok) sw2d_host::nccl().CommDestroy(h->comm_nccl);
 }
 
@@ -1017,6 +1029,44 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       left -= k;
     }
     return SW2D_OK;
+  }
+  // Small problems are bound by launch latency: replay a CUDA graph of
+  // kGraphPasses passes (same kernels and arguments, one graph per starting
+  // buffer parity) when there are no per-step diagnostics to address by step.
+  const int spl0 = !h->launches2.empty() ? 2 : 1;
+  const bool graphs = !h->multi && h->red_level == 0 && graphs_enabled();
+  while (graphs && nsteps >= (int64_t)kGraphPasses * spl0) {
+    cudaGraphExec_t& g = h->graph[h->cur];
+    if (!g || h->graph_spl != spl0) {
+      if (g) cudaGraphExecDestroy(g);
+      g = nullptr;
+      for (int b = 0; b < 2; ++b)
+        if (h->graph[b] && h->graph_spl != spl0) {
+          cudaGraphExecDestroy(h->graph[b]);
+          h->graph[b] = nullptr;
+        }
+      h->graph_spl = spl0;
+      const int cur0 = h->cur;
+      const int64_t steps0 = h->steps, launches0 = h->nlaunch;
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+      int rc = SW2D_OK;
+      for (int i = 0; i < kGraphPasses && rc == SW2D_OK; ++i) rc = run_pass(h, spl0);
+      const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
+      h->cur = cur0;  // capture only recorded the passes
+      h->steps = steps0;
+      h->nlaunch = launches0;
+      if (rc) return rc;
+      CUDA_TRY(h, ce);
+      const cudaError_t ie = cudaGraphInstantiate(&g, graph, 0);
+      cudaGraphDestroy(graph);
+      CUDA_TRY(h, ie);
+    }
+    CUDA_TRY(h, cudaGraphLaunch(g, h->stream));
+    h->nlaunch += (int64_t)kGraphPasses * (int64_t)(h->launches2.empty() ? h->launches.size()
+                                                                        : h->launches2.size());
+    h->steps += (int64_t)kGraphPasses * spl0;
+    nsteps -= (int64_t)kGraphPasses * spl0;  // kGraphPasses is even: parity unchanged
   }
   while (nsteps > 0) {
     const int spl = (nsteps >= 2 && !h->launches2.empty()) ? 2 : 1;

@@ -478,3 +478,16 @@ def test_virtual_ranks_kinds_bitwise(nranks, n, two, halo, monkeypatch):
             ref = np.zeros(oracle.NRED)
             ref[op] = want[4][k, op]
             check_reductions(row, ref)
+
+
+@pytest.mark.parametrize("kind", ["1", "2"])
+def test_graph_replay_both_parities(kind, monkeypatch):
+    """Long sw2d_step calls replay captured CUDA graphs (one per starting
+    buffer parity); chunks that start on either parity and leave remainders
+    equal the oracle bitwise."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", kind)
+    cfg, st = _bowl(300, 170)
+    n = 1 + 64 + 129 + 70
+    want = oracle_run(P, st, n)
+    got, _, _, launches = gpu_run(P, st, n, chunks=[1, 64, 129, 70])
+    assert_state_equal(got, want, where=f"graphs kind {kind}")
