@@ -322,14 +322,21 @@ def run_ours(args, cfg, ws, rank, local):
         alg_bytes = bpc * cells_local            # state in + state out, per launch
         hbm_achieved = alg_bytes / t_launch_s / 1e9
         peak, peak_src = hbm_peak()
-        kname = ("sw2d_step_cta2<%d>" if spl == 2 else "sw2d_step_cta<%d, 0>") % red_lvl
+        plan = dict(kv.split("=") for kv in sw2d.sw2d_plan(h).split())
+        if spl == 2:
+            kname = "sw2d_step_cta2<%d>" % red_lvl
+        elif plan.get("kernel") == "small":
+            kname = "sw2d_step_small<%d>" % red_lvl
+        else:
+            kname = "sw2d_step_cta<%d, 0>" % red_lvl
         if args.variant != "fused":
             kname = "paper_momentum + paper_continuity + paper_shapiro_update (per step)"
         hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s",
                "frac": hbm_achieved / peak, "peak_source": peak_src,
                "traffic": ncu_traffic(cfg["name"], kname) if args.variant == "fused" else None,
                "algorithmic_bytes_per_launch": alg_bytes, "model_steps_per_launch": spl}
-        roof = dict(hbm, kernel=kname, launches_per_model_step=launches_per_step)
+        roof = dict(hbm, kernel=kname, launches_per_model_step=launches_per_step,
+                    plan=sw2d.sw2d_plan(h))
         ipc = ncu_instr_per_cell_step(kname)
         if spl == 2 and ipc:
             # two steps per launch move 14 B per cell-step: the launch is bound by
@@ -345,7 +352,8 @@ def run_ours(args, cfg, ws, rank, local):
                     "peak_source": "4 warp-instructions/clk/SM x 32 x %d SMs x %.0f MHz "
                                    "(B200_PROFILING.md / B300_MICROARCH.md issue model)"
                                    % (sms, sm_hz / 1e6),
-                    "launches_per_model_step": launches_per_step, "hbm_view": hbm}
+                    "launches_per_model_step": launches_per_step, "hbm_view": hbm,
+                    "plan": sw2d.sw2d_plan(h)}
 
         # --- periodic output overlapped with compute (optional) ------------
         snaps = None

@@ -204,6 +204,11 @@ int sw2d_sync(sw2d* h);
  * -1 if h is NULL. */
 int64_t sw2d_launch_count(const sw2d* h);
 
+/* One-line description of the step plan this handle runs (kernel family,
+ * model steps per launch, launches per pass, strips, CTAs per SM, halo mode);
+ * owned by the handle, valid until sw2d_destroy.  "" if h is NULL. */
+const char* sw2d_plan(const sw2d* h);
+
 /* Destroy the handle and free its device memory / communicator.  NULL-safe. */
 void sw2d_destroy(sw2d* h);
 

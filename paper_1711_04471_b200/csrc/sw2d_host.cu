@@ -100,6 +100,7 @@ struct sw2d {
   // one per starting buffer parity; replayed for long sw2d_step calls
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int graph_spl = 0;
+  std::string plan_text;  // sw2d_plan()
   int sticky = 0;
   std::string err;
   ncclComm_t comm_nccl = nullptr;
@@ -280,6 +281,17 @@ void plan_launches(sw2d* h) {
     h->step_blocks2 = plan(h->launches2, per2, std::max(1LL, (long long)sms / ncc2), 8, 3);
   }
   plan_tb(h, sms);
+  {
+    static const char* kinds[] = {"warp-ring", "cta-ring", "small"};
+    char buf[256];
+    std::snprintf(buf, sizeof(buf),
+                  "kernel=%s steps_per_launch=%d launches_per_pass=%zu strips=%d "
+                  "ctas_per_sm=%d halo=%s temporal_blocking=%d",
+                  kinds[h->kind], h->launches2.empty() ? 1 : 2,
+                  h->launches2.empty() ? h->launches.size() : h->launches2.size(), h->nstrips,
+                  bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k);
+    h->plan_text = buf;
+  }
   if (std::getenv("SW2D_VERBOSE")) {
     if (h->tb_k)
       std::fprintf(stderr, "[sw2d] temporal blocking: %dx%d tiles, %d steps per launch\n",
@@ -1237,6 +1249,8 @@ int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
 }
 
 int64_t sw2d_launch_count(const sw2d* h) { return h ? h->nlaunch : -1; }
+
+const char* sw2d_plan(const sw2d* h) { return h ? h->plan_text.c_str() : ""; }
 
 void sw2d_destroy(sw2d* h) {
   if (!h) return;

@@ -32,7 +32,7 @@ SW2D_HALO_NCCL, SW2D_HALO_P2P = 0, 1
 SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",
            "sw2d_create", "sw2d_local_rows", "sw2d_set_state", "sw2d_step",
            "sw2d_run_snapshots", "sw2d_reduce", "sw2d_reduce_history", "sw2d_get_state",
-           "sw2d_sync",
+           "sw2d_sync", "sw2d_plan",
            "sw2d_launch_count", "sw2d_destroy", "sw2d_strerror",
            "sw2d_last_error")
 
@@ -88,6 +88,7 @@ def load(path: str = _LIB_PATH):
         "sw2d_get_state": ([vp, vp, vp, vp, vp], ctypes.c_int),
         "sw2d_sync": ([vp], ctypes.c_int),
         "sw2d_launch_count": ([vp], ctypes.c_int64),
+        "sw2d_plan": ([vp], ctypes.c_char_p),
         "sw2d_destroy": ([vp], None),
         "sw2d_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "sw2d_last_error": ([vp], ctypes.c_char_p),
@@ -231,6 +232,10 @@ def sw2d_sync(h) -> None:
 
 def sw2d_launch_count(h) -> int:
     return int(load().sw2d_launch_count(h))
+
+
+def sw2d_plan(h) -> str:
+    return load().sw2d_plan(h).decode()
 
 
 def sw2d_destroy(h) -> None:
