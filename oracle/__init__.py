@@ -1,4 +1,5 @@
-"""oracle — TEST INFRASTRUCTURE ONLY: the CPU parity oracle of the 2DSW step.
+"""oracle — TEST INFRASTRUCTURE ONLY: the CPU parity oracles of the 2DSW step
+and (NEXT-4) of red-black SOR for the Poisson equation.
 
 Plain single-threaded C11 (``oracle/sw2d_ref.c``), loaded with ctypes.  It
 follows arXiv 1711.04471 §6.2 (time loop -> predictor
@@ -22,6 +23,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sw2d_ref.c")
+_SOR_SRC = os.path.join(_HERE, "sor_ref.c")   # NEXT-4: red-black SOR Poisson
 _LIB = os.path.join(_HERE, "libsw2d_ref.so")
 
 # reduction slots (sw2d_ref.h)
@@ -37,10 +39,10 @@ CFLAGS = ["-std=c11", "-O2", "-fPIC", "-shared", "-ffp-contract=off",
 def build(force: bool = False) -> str:
     """Compile libsw2d_ref.so (gcc, no FMA contraction, no fast-math)."""
     if force or not os.path.exists(_LIB) or (
-            os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC),
+            os.path.getmtime(_LIB) < max(os.path.getmtime(_SRC), os.path.getmtime(_SOR_SRC),
                                          os.path.getmtime(_SRC[:-1] + "h"))):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, _SOR_SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -49,6 +51,11 @@ class _Params(ctypes.Structure):
     _fields_ = [("dx", ctypes.c_float), ("dy", ctypes.c_float),
                 ("dt", ctypes.c_float), ("g", ctypes.c_float),
                 ("eps", ctypes.c_float), ("hmin", ctypes.c_float)]
+
+
+class _SorParams(ctypes.Structure):
+    _fields_ = [("dx", ctypes.c_float), ("dy", ctypes.c_float), ("dz", ctypes.c_float),
+                ("omega", ctypes.c_float)]
 
 
 _lib = None
@@ -67,7 +74,10 @@ def _load():
                                         fp, fp, fp, dp]
         lib.sw2d_ref_wet.argtypes = [ctypes.POINTER(_Params), i64, i64, fp, fp,
                                      ctypes.POINTER(ctypes.c_uint8)]
-        for f in (lib.sw2d_ref_run, lib.sw2d_ref_reduce, lib.sw2d_ref_wet):
+        lib.sor_ref_run.argtypes = [ctypes.POINTER(_SorParams), i64, i64, i64, fp, fp, i64, dp]
+        lib.sor_ref_residual.argtypes = [ctypes.POINTER(_SorParams), i64, i64, i64, fp, fp, dp]
+        for f in (lib.sw2d_ref_run, lib.sw2d_ref_reduce, lib.sw2d_ref_wet, lib.sor_ref_run,
+                  lib.sor_ref_residual):
             f.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -130,4 +140,38 @@ def wet(params, hzero, eta) -> np.ndarray:
                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
     if rc != 0:
         raise ValueError("sw2d_ref_wet: invalid arguments")
+    return out
+
+
+# --- NEXT-4: red-black SOR for the Poisson equation (oracle/sor_ref.c) -------
+
+def _sor_params(p) -> _SorParams:
+    return _SorParams(float(p["dx"]), float(p["dy"]), float(p["dz"]), float(p["omega"]))
+
+
+def sor_run(params, p, rhs, n: int, history: bool = False):
+    """n red-black SOR iterations from p (float32 [nz][ny][nx], copied) for
+    Lap(p) = rhs with zero Dirichlet ghosts; returns p (and, with history,
+    [n][2] float64: L2 and Linf of the residual after each iteration)."""
+    nz, ny, nx = np.shape(rhs)
+    pp, ptr = _f32(np.array(p, dtype=np.float32, copy=True))
+    rr, rptr = _f32(rhs)
+    hist = np.zeros((max(n, 0), 2), np.float64) if history else None
+    hp = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if history else None
+    prm = _sor_params(params)
+    if _load().sor_ref_run(ctypes.byref(prm), nx, ny, nz, ptr, rptr, int(n), hp) != 0:
+        raise ValueError("sor_ref_run: invalid arguments")
+    return (pp, hist) if history else pp
+
+
+def sor_residual(params, p, rhs) -> np.ndarray:
+    """[L2, Linf] of r = rhs - Lap(p)."""
+    nz, ny, nx = np.shape(rhs)
+    pp, ptr = _f32(p)
+    rr, rptr = _f32(rhs)
+    out = np.zeros(2, np.float64)
+    prm = _sor_params(params)
+    if _load().sor_ref_residual(ctypes.byref(prm), nx, ny, nz, ptr, rptr,
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))) != 0:
+        raise ValueError("sor_ref_residual: invalid arguments")
     return out
