@@ -52,7 +52,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [
-        os.path.join(ROOT, "include", "sw2d.h"), __file__]
+        os.path.join(ROOT, "include", "sw2d.h"), os.path.join(ROOT, "include", "sor3d.h"), __file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 

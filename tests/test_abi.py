@@ -86,3 +86,36 @@ def test_create_validates_params_before_touching_the_gpu(lib):
 def test_nccl_unique_id_host_only(lib):
     uid = sw2d.sw2d_nccl_unique_id()
     assert len(uid) == 128
+
+
+# --- NEXT-4: include/sor3d.h ---------------------------------------------------
+
+def _declared_sor3d():
+    src = open(os.path.join(ROOT, "include", "sor3d.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sor3d_[a-z_]+)\s*\(", src)))
+
+
+def test_sor3d_exports_every_declared_symbol(lib):
+    from paper_1711_04471_b200 import sor3d
+    declared = _declared_sor3d()
+    assert len(declared) >= 12
+    assert declared == sorted(sor3d.SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    src = open(os.path.join(ROOT, "include", "sor3d.h")).read()
+    assert sor3d.sor3d_abi_version() == int(
+        re.search(r"#define SOR3D_ABI_VERSION (\d+)", src).group(1))
+
+
+def test_sor3d_create_validates_params_before_touching_the_gpu(lib):
+    from paper_1711_04471_b200 import sor3d
+    for b in [dict(nx=0), dict(nz=-3), dict(dx=0.0), dict(dz=float("inf")), dict(omega=2.0),
+              dict(omega=0.0), dict(history_len=-1), dict(ny=(1 << 20) + 1)]:
+        kw = dict(nx=8, ny=8, nz=8)
+        kw.update(b)
+        with pytest.raises(sor3d.Sor3dError) as ei:
+            sor3d.sor3d_create(sor3d.make_params(**kw))
+        assert ei.value.code == sor3d.SOR3D_EINVAL
+    assert sor3d.sor3d_launch_count(None) == -1
+    assert sor3d.sor3d_history_count(None) == -1
