@@ -20,6 +20,13 @@ bench step uploads the state from pinned host memory (sw2d_set_state), runs
 T steps and reads the T per-step volumes back (sw2d_reduce_history).
 `--impl reference`: the CPU oracle (oracle/, single-threaded C) timed on a
 bounded sample of the same workload (rank 0 only).
+
+`--workload sor300|sor1024`: the paper's second
+workload, red-black SOR for the UFLES pressure Poisson equation
+ through include/sor3d.h: one bench step = one
+sor3d_iterate(50) call (the paper's 50 SOR iterations per time step) with the
+residual folded every iteration; metric SOR cell-iterations/s.  L2 is flushed
+(a 512 MB write) before every timed step, each step timed by its own events.
 """
 from __future__ import annotations
 
@@ -51,7 +58,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4", "p1000", "p2000"], default="c5")
+    ap.add_argument("--workload", choices=["c5", "c3", "c2", "c1", "c4", "p1000", "p2000",
+                                           "sor300", "sor1024"], default="c5")
+    ap.add_argument("--sor-iters", type=int, default=None,
+                    help="SOR iterations per bench step (default: the config's, 50 for sor300)")
+    ap.add_argument("--sor-residual-every", type=int, default=1,
+                    help="SOR residual fold every N iterations (0: none)")
     ap.add_argument("--substeps", type=int, default=None,
                     help="model time steps per bench step (default 100; c2: 10000)")
     ap.add_argument("--reduce", choices=["default", "none", "volume", "all"], default="default",
@@ -434,9 +446,195 @@ def run_ours(args, cfg, ws, rank, local):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# NEXT-4: red-black SOR (include/sor3d.h)
+# ---------------------------------------------------------------------------
+
+SOR_METRIC = "SOR cell-iterations/s (red-black 7-point Poisson, UFLES press shape)"
+SOR_UNIT = "cell-iterations/s"
+SOR_BYTES_PER_CELL = 12      # one fused iteration: read p, rhs (8 B) + write p (4 B)
+SOR_RES_BYTES_PER_CELL = 8   # the trailing residual-only pass: read p, rhs
+
+
+def sor_config(cfg, args, n, every):
+    return {
+        "workload": f"{cfg['name']}: {cfg['desc']}",
+        "nx": cfg["nx"], "ny": cfg["ny"], "nz": cfg["nz"], "iterations_per_step": n,
+        "residual_every": every, "omega": 1.5, "dx": 4.0, "dz": 2.0,
+        "parallelism": "1 GPU (replicas only: independent solves per GPU)",
+        "l2": "L2 flushed (512 MB write) before every timed step; each step timed alone",
+    }
+
+
+def run_sor_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    import oracle
+    import sor_inputs as so
+    p0, rhs = so.generate(cfg)
+    prm = so.params()
+    n = min(args.sor_iters or cfg["iters"], 10)
+    hist = args.sor_residual_every > 0
+    for _ in range(max(args.warmup, 0)):
+        oracle.sor_run(prm, p0, rhs, 1, history=hist)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.sor_run(prm, p0, rhs, n, history=hist)
+        times.append(time.perf_counter() - t)
+    tot = sum(times)
+    cells = so.cells(cfg)
+    value = cells * n * args.steps / tot
+    desc = (f"the full {cfg['nx']}x{cfg['ny']}x{cfg['nz']} grid, {n} iterations per step "
+            f"(residual every iteration: {hist}), single-threaded C oracle")
+    print(json.dumps({
+        "impl": "reference", "metric": SOR_METRIC, "value": value, "unit": SOR_UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": sor_config(cfg, args, n, args.sor_residual_every),
+        "cpu_baseline": {"value": value, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": SOR_UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_sor_ours(args, cfg, ws, rank, local):
+    """Replicas only: every rank solves its own copy (no data-path exchange)."""
+    import torch
+    import torch.distributed as dist
+
+    import sor_inputs as so
+    from paper_1711_04471_b200 import sor3d
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nx, ny, nz = cfg["nx"], cfg["ny"], cfg["nz"]
+    cells = nx * ny * nz
+    n = args.sor_iters or cfg["iters"]
+    every = args.sor_residual_every
+    nrec = 0 if every <= 0 else len([t for t in range(1, n + 1) if t % every == 0 or t == n])
+    p0, rhs = so.generate(cfg)
+    hp0 = torch.from_numpy(p0).pin_memory()
+    hrhs = torch.from_numpy(rhs).pin_memory()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    h = sor3d.sor3d_create(sor3d.make_params(nx, ny, nz, **so.params(),
+                                             history_len=max(nrec, 1)), stream)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed_steps(body):
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.fill_(1)                      # L2 flush, outside the timed region
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            body()
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        return tot
+
+    try:
+        sor3d.sor3d_set(h, hp0, hrhs)
+        for _ in range(args.warmup):
+            sor3d.sor3d_iterate(h, n, every)
+        sor3d.sor3d_sync(h)
+        l0 = sor3d.sor3d_launch_count(h)
+        with Clocks(local) as clk:
+            barrier()
+            torch.cuda.synchronize()
+            ms = timed_steps(lambda: sor3d.sor3d_iterate(h, n, every))
+            torch.cuda.synchronize()
+            barrier()
+        ms = max_over_ranks(ms)
+        launches = sor3d.sor3d_launch_count(h) - l0
+        value = ws * cells * n * args.steps / (ms * 1e-3)
+        step_s = ms * 1e-3 / args.steps
+        alg = cells * (SOR_BYTES_PER_CELL * n + (SOR_RES_BYTES_PER_CELL if every > 0 else 0))
+        peak, peak_src = hbm_peak()
+        kname = "sor_iter<32, %d, 1, %d>" % (1 if every > 0 else 0,
+                                           1 if "L2 hints" in sor3d.sor3d_plan(h) else 0)
+        ach = alg / step_s / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "peak_source": peak_src,
+                "traffic": ncu_traffic(cfg["name"], kname), "kernel": kname,
+                "algorithmic_bytes_per_step": alg,
+                "algorithmic_bytes_per_cell_iteration": SOR_BYTES_PER_CELL,
+                "launches_per_step": launches / args.steps, "plan": sor3d.sor3d_plan(h)}
+
+        e2e = None
+        if not args.no_e2e and not args.profile:
+            hist = np.empty((max(nrec, 1), 2), np.float64)
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+
+            def e2e_body():
+                sor3d.sor3d_set(h, hp0, hrhs)
+                sor3d.sor3d_iterate(h, n, every)
+                if nrec:
+                    hist[:] = sor3d.sor3d_residual_history(h, nrec)
+                else:
+                    sor3d.sor3d_residual(h)
+            ems = max_over_ranks(timed_steps(e2e_body))
+            e2e = {"value": ws * cells * n * args.steps / (ems * 1e-3), "unit": SOR_UNIT,
+                   "h2d_bytes_per_step": 8 * cells, "d2h_bytes_per_step": 16 * max(nrec, 1),
+                   "ms_per_step": ems / args.steps, "wall_s": time.perf_counter() - t0,
+                   "path": "sor3d_set(pinned host p, rhs) + sor3d_iterate(n, every) + "
+                           "sor3d_residual_history per bench step"}
+    finally:
+        sor3d.sor3d_destroy(h)
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline and not args.profile:
+        import oracle
+        ns = 10
+        t = time.perf_counter()
+        oracle.sor_run(so.params(), p0, rhs, ns, history=every > 0)
+        dt_s = time.perf_counter() - t
+        cpu = {"value": cells * ns / dt_s, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"the full grid, {ns} iterations (residual every iteration: "
+                         f"{every > 0}), single-threaded C oracle", "seconds": dt_s}
+    print(json.dumps({
+        "metric": SOR_METRIC, "value": value, "unit": SOR_UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded Gaussian sources + noise, sor_inputs)",
+        "config": sor_config(cfg, args, n, every), "roofline": roof, "cpu_baseline": cpu,
+        "e2e": e2e, "clocks": clk.summary(), "gpu_launches": launches,
+    }), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if args.workload.startswith("sor"):
+        import sor_inputs as so
+        cfg = so.config(args.workload)
+        if args.impl == "reference":
+            run_sor_reference(args, cfg, rank)
+        else:
+            run_sor_ours(args, cfg, ws, rank, local)
+        return
     if args.substeps is None:
         args.substeps = default_substeps(args.workload)
     cfg = si.config(args.workload, ws if args.workload == "c5" else 1)

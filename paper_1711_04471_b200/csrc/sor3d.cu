@@ -189,6 +189,12 @@ __device__ __forceinline__ void sth(float* p, float4 v) {
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(l2pol<true>()) : "memory");
 }
 
+__device__ __forceinline__ float4 lds4(const float4* p) { return *p; }
+
+#ifndef SOR_MINB
+#define SOR_MINB(R) (64 / (R))  // 1024 threads per SM: at most 64 registers
+#endif
+
 // Per-thread state of the z-march: p_in planes m-1 .. m+2, rhs planes
 // m-1 .. m+2, new (red-updated) planes m-2, m-1, and the stream pointers.
 struct March {
@@ -214,9 +220,8 @@ struct Lane {
   int k0, k1;    // output planes
   int nz;
   long long plane;
-  bool rok[4];   // red update allowed at cell c (tile + apron 1, interior)
-  bool ook[4];   // output cell c (tile, interior)
-  bool all4;     // all four cells are output cells
+  int intr;      // bit c: cell c is an interior cell (the red update applies)
+  int outm;      // bit c: cell c is an output cell (tile, interior): stored
   int tx, ty;
   int yn, ys;
 };
@@ -233,47 +238,54 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
   // of the buffers the step writes (last read in step m-1).
   s_in[S][ty][tx] = st.pz1;
   __syncthreads();
-  const float4 N = s_in[S][L.yn][tx], S4 = s_in[S][L.ys][tx];
-  // x neighbours outside the lane's float4
-  const float wl = __shfl_up_sync(kFull, st.pz1.w, 1, kSx);
-  const float er = __shfl_down_sync(kFull, st.pz1.x, 1, kSx);
+  const float4 N = lds4(&s_in[S][L.yn][tx]), S4 = lds4(&s_in[S][L.ys][tx]);
+  // the x neighbour outside the lane's quad: W of cell 0 (P = 0) or E of cell 3
+  const float xo = P == 0 ? __shfl_up_sync(kFull, st.pz1.w, 1, kSx)
+                          : __shfl_down_sync(kFull, st.pz1.x, 1, kSx);
   float4 pn = st.pz1;
   const bool mint = m >= 1 && m <= L.nz;
-  const bool rstep = RES && m >= L.k0 && m <= L.k1;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const bool upd_here = (c & 1) == P;
     if (!upd_here && !RES) continue;
-    const float W = c == 0 ? wl : compv(st.pz1, c - 1);
-    const float E = c == 3 ? er : compv(st.pz1, c + 1);
+    float W, E;
+    if (upd_here) {
+      W = c == 0 ? xo : compv(st.pz1, c - 1);
+      E = c == 3 ? xo : compv(st.pz1, c + 1);
+    } else {  // residual only: the other two cells (their x neighbours are in the quad or shuffled)
+      W = c == 0 ? __shfl_up_sync(kFull, st.pz1.w, 1, kSx) : compv(st.pz1, c - 1);
+      E = c == 3 ? __shfl_down_sync(kFull, st.pz1.x, 1, kSx) : compv(st.pz1, c + 1);
+    }
     const float ns = nsum(E, W, compv(N, c), compv(S4, c), compv(st.pz2, c), compv(st.pz0, c), a);
-    if (upd_here && mint && L.rok[c]) comp(pn, c) = upd(compv(st.pz1, c), ns, compv(st.r2, c), a);
-    if (RES && rstep && L.ook[c]) {
+    // red update of interior cells (apron cells outside the box are never read)
+    if (upd_here && mint && (L.intr >> c & 1)) comp(pn, c) = upd(compv(st.pz1, c), ns, compv(st.r2, c), a);
+    if (RES && m >= L.k0 && m <= L.k1 && (L.outm >> c & 1)) {
       const float r = __fsub_rn(compv(st.r2, c), __fsub_rn(ns, __fmul_rn(a.dd, compv(st.pz1, c))));
-      st.acc += (double)r * (double)r;
+      st.acc = fma((double)r, (double)r, st.acc);
       st.amx = fmaxf(st.amx, fabsf(r));
     }
   }
   if (WRITE) {
     s_new[S][ty][tx] = pn;  // read by the black phase of step m+1
-    const float4 Nb = s_new[S ^ 1][L.yn][tx], Sb = s_new[S ^ 1][L.ys][tx];
-    const float wb = __shfl_up_sync(kFull, st.n1.w, 1, kSx);
-    const float eb = __shfl_down_sync(kFull, st.n1.x, 1, kSx);
+    const float4 Nb = lds4(&s_new[S ^ 1][L.yn][tx]), Sb = lds4(&s_new[S ^ 1][L.ys][tx]);
+    const float xb = P == 0 ? __shfl_up_sync(kFull, st.n1.w, 1, kSx)
+                            : __shfl_down_sync(kFull, st.n1.x, 1, kSx);
     if (m - 1 >= L.k0 && m - 1 <= L.k1) {
+      // black cells of plane m-1 (computed everywhere, stored on output cells)
       float4 o = st.n1;
 #pragma unroll
       for (int c = P; c < 4; c += 2) {
-        const float W = c == 0 ? wb : compv(st.n1, c - 1);
-        const float E = c == 3 ? eb : compv(st.n1, c + 1);
+        const float W = c == 0 ? xb : compv(st.n1, c - 1);
+        const float E = c == 3 ? xb : compv(st.n1, c + 1);
         const float ns = nsum(E, W, compv(Nb, c), compv(Sb, c), compv(pn, c), compv(st.n0, c), a);
-        if (L.ook[c]) comp(o, c) = upd(compv(st.n1, c), ns, compv(st.r1, c), a);
+        comp(o, c) = upd(compv(st.n1, c), ns, compv(st.r1, c), a);
       }
-      if (L.all4) {
+      if (L.outm == 15) {
         sth<H>(st.op, o);
-      } else {
+      } else if (L.outm) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (L.ook[c]) st.op[c] = compv(o, c);
+          if (L.outm >> c & 1) st.op[c] = compv(o, c);
       }
     }
   }
@@ -309,7 +321,7 @@ __device__ __forceinline__ void march(March& st, const Lane& L, const Args& a, i
 // residual-only pass).  Thread (tx, ty) holds the x-quad x = 4tx .. 4tx+3 of
 // row y = ty of the extended 128 x 16 tile.
 template <int R, bool RES, bool WRITE, bool H>
-__global__ void __launch_bounds__(kSx * R, 64 / R) sor_iter(const Args a) {
+__global__ void __launch_bounds__(kSx * R, SOR_MINB(R)) sor_iter(const Args a) {
   __shared__ float4 s_in[2][R][kSx];
   __shared__ float4 s_new[2][R][kSx];
   // Row of the extended tile: a warp holds two rows of equal parity (half-warp
@@ -327,16 +339,15 @@ __global__ void __launch_bounds__(kSx * R, 64 / R) sor_iter(const Args a) {
   L.nz = a.nz;
   L.plane = a.plane;
   const bool rowin = j >= 1 && j <= a.ny;
-  const bool boxy = ty >= 1 && ty <= R - 2;
   const bool outy = ty >= 2 && ty <= R - 3;
-  L.all4 = true;
+  L.intr = 0;
+  L.outm = 0;
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const int x = 4 * tx + c, i = i0 + c;
     const bool in = rowin && i >= 1 && i <= a.nx;
-    L.rok[c] = in && boxy && x >= 1 && x <= 4 * kSx - 2;
-    L.ook[c] = in && outy && x >= 2 && x <= 4 * kSx - 3;
-    L.all4 = L.all4 && L.ook[c];
+    if (in) L.intr |= 1 << c;
+    if (in && outy && x >= 2 && x <= 4 * kSx - 3) L.outm |= 1 << c;
   }
   L.tx = tx;
   L.ty = ty;

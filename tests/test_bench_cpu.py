@@ -43,3 +43,16 @@ def test_reference_arm_torchrun_two_ranks():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+
+
+def test_reference_arm_sor_workload():
+    """NEXT-4: the SOR workload's reference arm (the SOR oracle)."""
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "sor300",
+                        "--steps", "1", "--warmup", "0", "--sor-iters", "1"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = _lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert KEYS <= set(d), KEYS - set(d)
+    assert d["unit"] == "cell-iterations/s" and d["config"]["nz"] == 90 and d["value"] > 0
