@@ -403,6 +403,7 @@ struct sor3d {
   unsigned* counter = nullptr;
   double* hist = nullptr;  // [cap][2]
   double* scratch = nullptr;  // [2] for sor3d_residual
+  float* stage = nullptr;     // dense staging buffer for host uploads/downloads (lazy)
   int cap = 0;
   int rows_cta = 32;  // extended tile rows (CTA = 16 x rows_cta threads)
   bool hint = false;  // L2 eviction hints (p and rhs fit in L2)
@@ -518,33 +519,36 @@ double* next_record(sor3d* h) {
   return r;
 }
 
-cudaMemcpy3DParms copy_parms(sor3d* h, float* dev, const float* host, bool to_dev) {
-  cudaMemcpy3DParms c;
-  std::memset(&c, 0, sizeof(c));
-  const cudaPitchedPtr dp =
-      make_cudaPitchedPtr(dev, (size_t)h->pitch * sizeof(float), (size_t)h->pitch, (size_t)h->rows);
-  const cudaPitchedPtr hp = make_cudaPitchedPtr(const_cast<float*>(host), (size_t)h->nx * sizeof(float),
-                                                (size_t)h->nx, (size_t)h->ny);
-  const cudaPos dpos = make_cudaPos((size_t)(1 + kColOff) * sizeof(float), (size_t)(1 + kRowOff),
-                                    (size_t)(1 + kPlaneOff));
-  if (to_dev) {
-    c.srcPtr = hp;
-    c.dstPtr = dp;
-    c.dstPos = dpos;
-  } else {
-    c.srcPtr = dp;
-    c.srcPos = dpos;
-    c.dstPtr = hp;
+// Dense [nz][ny][nx] <-> padded storage, one grid-stride pass: TO_PAD also
+// counts non-finite values (sor3d_set's check).
+template <bool TO_PAD>
+__global__ void repack(float* pad, const float* din, float* dout, int nx, int ny, long long rows,
+                       long long pitch, long long plane, unsigned* bad) {
+  unsigned nb = 0;
+  for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+    const long long k = row / ny, j = row % ny;
+    const long long po = (k + 1 + kPlaneOff) * plane + (j + 1 + kRowOff) * pitch + 1 + kColOff;
+    const long long dofs = row * nx;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      if (TO_PAD) {
+        const float v = din[dofs + i];
+        nb += !isfinite(v);
+        pad[po + i] = v;
+      } else {
+        dout[dofs + i] = pad[po + i];
+      }
+    }
   }
-  c.extent = make_cudaExtent((size_t)h->nx * sizeof(float), (size_t)h->ny, (size_t)h->nz);
-  c.kind = cudaMemcpyDefault;
-  return c;
+  if (TO_PAD && nb) atomicAdd(bad, nb);
 }
 
-__global__ void count_nonfinite(const float* a, long long n, unsigned* bad) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    if (!isfinite(a[i])) atomicAdd(bad, 1u);
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
 void free_all(sor3d* h) {
@@ -555,7 +559,26 @@ void free_all(sor3d* h) {
   cudaFree(h->counter);
   cudaFree(h->hist);
   cudaFree(h->scratch);
+  cudaFree(h->stage);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+}
+
+// host arrays go through a dense device staging buffer (one contiguous copy)
+// and a repack kernel; device arrays are repacked directly
+int upload(sor3d* h, float* pad, const float* src, unsigned* bad) {
+  const long long n = h->nx * h->ny * h->nz;
+  const float* d = src;
+  if (!is_device_ptr(src)) {
+    if (!h->stage) SOR_TRY(h, cudaMalloc(&h->stage, (size_t)n * sizeof(float)));
+    SOR_TRY(h, cudaMemcpyAsync(h->stage, src, (size_t)n * sizeof(float), cudaMemcpyDefault,
+                               h->stream));
+    d = h->stage;
+  }
+  const long long rows = h->ny * h->nz;
+  repack<true><<<(unsigned)std::min<long long>(rows, 148 * 16), 256, 0, h->stream>>>(
+      pad, d, nullptr, (int)h->nx, (int)h->ny, rows, h->pitch, h->plane, bad);
+  SOR_TRY(h, cudaGetLastError());
+  return SOR3D_OK;
 }
 
 }  // namespace
@@ -697,24 +720,18 @@ int sor3d_create(const sor3d_params* prm, void* cuda_stream, sor3d** out) {
 int sor3d_set(sor3d* h, const float* p, const float* rhs) {
   SOR_ENTER(h);
   if (!rhs) return fail(h, SOR3D_EINVAL, "rhs is NULL");
-  const size_t bytes = (size_t)h->plane * (size_t)h->planes * sizeof(float);
-  SOR_TRY(h, cudaMemsetAsync(h->p[0], 0, bytes, h->stream));
-  SOR_TRY(h, cudaMemsetAsync(h->p[1], 0, bytes, h->stream));
-  SOR_TRY(h, cudaMemsetAsync(h->rhs, 0, bytes, h->stream));
-  SOR_TRY(h, cudaStreamSynchronize(h->stream));
-  cudaMemcpy3DParms c = copy_parms(h, h->rhs, rhs, true);
-  SOR_TRY(h, cudaMemcpy3D(&c));
-  if (p) {
-    c = copy_parms(h, h->p[0], p, true);
-    SOR_TRY(h, cudaMemcpy3D(&c));
-  }
-  // non-finite check on the device copies (padding is zero)
+  h->have_state = false;
   unsigned* bad = reinterpret_cast<unsigned*>(h->scratch);
   SOR_TRY(h, cudaMemsetAsync(bad, 0, sizeof(unsigned), h->stream));
-  const long long n = h->plane * h->planes;
-  count_nonfinite<<<592, 256, 0, h->stream>>>(h->rhs, n, bad);
-  count_nonfinite<<<592, 256, 0, h->stream>>>(h->p[0], n, bad);
-  SOR_TRY(h, cudaGetLastError());
+  int rc = upload(h, h->rhs, rhs, bad);
+  if (rc) return rc;
+  if (p) {
+    rc = upload(h, h->p[0], p, bad);
+    if (rc) return rc;
+  } else {  // p = 0 (the padding is zero already)
+    SOR_TRY(h, cudaMemsetAsync(h->p[0], 0, (size_t)h->plane * (size_t)h->planes * sizeof(float),
+                               h->stream));
+  }
   unsigned nb = 0;
   SOR_TRY(h, cudaMemcpyAsync(&nb, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, h->stream));
   SOR_TRY(h, cudaStreamSynchronize(h->stream));
@@ -771,9 +788,16 @@ int sor3d_get(sor3d* h, float* p) {
   SOR_ENTER(h);
   if (!p) return fail(h, SOR3D_EINVAL, "p is NULL");
   if (!h->have_state) return fail(h, SOR3D_ESTATE, "sor3d_get before sor3d_set");
+  const long long n = h->nx * h->ny * h->nz, rows = h->ny * h->nz;
+  const bool dev = is_device_ptr(p);
+  if (!dev && !h->stage) SOR_TRY(h, cudaMalloc(&h->stage, (size_t)n * sizeof(float)));
+  float* d = dev ? p : h->stage;
+  repack<false><<<(unsigned)std::min<long long>(rows, 148 * 16), 256, 0, h->stream>>>(
+      h->p[h->cur], nullptr, d, (int)h->nx, (int)h->ny, rows, h->pitch, h->plane, nullptr);
+  SOR_TRY(h, cudaGetLastError());
+  if (!dev)
+    SOR_TRY(h, cudaMemcpyAsync(p, d, (size_t)n * sizeof(float), cudaMemcpyDefault, h->stream));
   SOR_TRY(h, cudaStreamSynchronize(h->stream));
-  cudaMemcpy3DParms c = copy_parms(h, h->p[h->cur], p, false);
-  SOR_TRY(h, cudaMemcpy3D(&c));
   return SOR3D_OK;
 }
 
