@@ -80,6 +80,14 @@ struct sw2d {
   RedPartial* partials = nullptr;
   int partials_cap = 0;
   unsigned int* counter = nullptr;
+  // CUDA graphs with per-step diagnostics: a captured pass writes its records
+  // to grec[step within the graph]; the graph ends with ring_scatter, which
+  // moves them to the history ring at the device step counter *dstep.
+  double* grec = nullptr;
+  unsigned long long* dstep = nullptr;
+  bool capturing = false;
+  int cap_step = 0;
+  int64_t dstep_host = -1;  // value *dstep will hold when the queued work reaches it (-1: unknown)
   double* hist = nullptr;
   int hist_len = 0;
   double* rec = nullptr;    // scratch record (ingest, sw2d_reduce)
@@ -533,6 +541,8 @@ void free_all(sw2d* h) {
   h->slabs.clear();
   cudaFree(h->partials);
   cudaFree(h->counter);
+  cudaFree(h->dstep);
+  cudaFree(h->grec);
   cudaFree(h->hist);
   cudaFree(h->rec);
   cudaFree(h->h0sum);
@@ -706,6 +716,8 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   h->partials_cap = (int)cap;
   CUDA_TRY(h, cudaMalloc(&h->partials, sizeof(RedPartial) * (size_t)cap));
   CUDA_TRY(h, cudaMalloc(&h->counter, 2 * sizeof(unsigned int)));
+  CUDA_TRY(h, cudaMalloc(&h->dstep, sizeof(unsigned long long)));
+  CUDA_TRY(h, cudaMalloc(&h->grec, sizeof(double) * kRecN * 2 * (size_t)kGraphPasses));
   CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, 2 * sizeof(unsigned int), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
   CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
@@ -737,6 +749,20 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
 // launches (phase 0, overlapping the exchange), the boundary launches
 // (phase 1; in P2P mode they also store their rows into the neighbours'
 // halos), the neighbours' signal, and the per-step diagnostics' allreduce.
+__global__ void set_dstep(unsigned long long* dstep, unsigned long long v) { *dstep = v; }
+
+// end of a replayed graph: its n records go to history slots (*dstep + i) % len
+__global__ void ring_scatter(const double* grec, double* hist, int len,
+                             unsigned long long* dstep, int n) {
+  const unsigned long long s0 = *dstep;
+  for (int t = threadIdx.x; t < n * kRecN; t += blockDim.x) {
+    const int i = t / kRecN, f = t % kRecN;
+    hist[(size_t)((s0 + (unsigned long long)i) % (unsigned long long)len) * kRecN + f] = grec[t];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *dstep = s0 + (unsigned long long)n;
+}
+
 int run_pass(sw2d* h, int spl) {
   const bool p2p = h->halo_mode == SW2D_HALO_P2P && (h->virt || h->multi);
   const auto& mo = sw2d_host::memops();
@@ -744,8 +770,10 @@ int run_pass(sw2d* h, int spl) {
   const int blocks = spl == 2 ? h->step_blocks2 : h->step_blocks;
   double* rec[2];
   for (int k = 0; k < 2; ++k)
-    rec[k] = h->red_level ? h->hist + (size_t)((h->steps + k) % h->hist_len) * kRecN
-                          : h->rec + k * kRecN;
+    rec[k] = !h->red_level ? h->rec + k * kRecN
+             : h->capturing ? h->grec + (size_t)(h->cap_step + k) * kRecN
+                            : h->hist + (size_t)((h->steps + k) % h->hist_len) * kRecN;
+  if (h->capturing) h->cap_step += spl;
   if (h->virt && !p2p) {
     int rc = virtual_halo(h, h->cur);
     if (rc) return rc;
@@ -979,6 +1007,7 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
     }
     CUDA_TRY(h, cudaGetLastError());
   }
+  h->dstep_host = -1;
   int bad = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1044,9 +1073,10 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
   }
   // Small problems are bound by launch latency: replay a CUDA graph of
   // kGraphPasses passes (same kernels and arguments, one graph per starting
-  // buffer parity) when there are no per-step diagnostics to address by step.
+  // buffer parity); per-step diagnostics find their history slot on the
+  // device, so they replay too.
   const int spl0 = !h->launches2.empty() ? 2 : 1;
-  const bool graphs = !h->multi && h->red_level == 0 && graphs_enabled();
+  const bool graphs = !h->multi && graphs_enabled();
   while (graphs && nsteps >= (int64_t)kGraphPasses * spl0) {
     cudaGraphExec_t& g = h->graph[h->cur];
     if (!g || h->graph_spl != spl0) {
@@ -1063,7 +1093,13 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       cudaGraph_t graph = nullptr;
       CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
       int rc = SW2D_OK;
+      h->capturing = true;
+      h->cap_step = 0;
       for (int i = 0; i < kGraphPasses && rc == SW2D_OK; ++i) rc = run_pass(h, spl0);
+      h->capturing = false;
+      if (rc == SW2D_OK && h->red_level)
+        ring_scatter<<<1, 256, 0, h->stream>>>(h->grec, h->hist, h->hist_len, h->dstep,
+                                               kGraphPasses * spl0);
       const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
       h->cur = cur0;  // capture only recorded the passes
       h->steps = steps0;
@@ -1074,9 +1110,15 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       cudaGraphDestroy(graph);
       CUDA_TRY(h, ie);
     }
+    if (h->red_level && h->dstep_host != h->steps) {  // sync the device step counter
+      set_dstep<<<1, 1, 0, h->stream>>>(h->dstep, (unsigned long long)h->steps);
+      h->nlaunch++;
+    }
     CUDA_TRY(h, cudaGraphLaunch(g, h->stream));
     h->nlaunch += (int64_t)kGraphPasses * (int64_t)(h->launches2.empty() ? h->launches.size()
-                                                                        : h->launches2.size());
+                                                                        : h->launches2.size()) +
+                  (h->red_level ? 1 : 0);
+    if (h->red_level) h->dstep_host = h->steps + (int64_t)kGraphPasses * spl0;
     h->steps += (int64_t)kGraphPasses * spl0;
     nsteps -= (int64_t)kGraphPasses * spl0;  // kGraphPasses is even: parity unchanged
   }

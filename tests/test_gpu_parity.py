@@ -491,3 +491,60 @@ def test_graph_replay_both_parities(kind, monkeypatch):
     want = oracle_run(P, st, n)
     got, _, _, launches = gpu_run(P, st, n, chunks=[1, 64, 129, 70])
     assert_state_equal(got, want, where=f"graphs kind {kind}")
+
+
+def _history_run(st, chunks, mask, history_len, dist=None):
+    hz, e, u, v = st
+    ny, nx = hz.shape
+    p = sw2d.make_params(nx, ny, P["dx"], P["dy"], P["dt"], P["g"], P["eps"], P["hmin"],
+                         reduce_every_step=mask, history_len=history_len)
+    h = sw2d.sw2d_create(p, dist)
+    try:
+        sw2d.sw2d_set_state(h, hz, e, u, v)
+        for n in chunks:
+            sw2d.sw2d_step(h, n)
+        out = sw2d.get_state(h, nx)
+        k = min(sum(chunks), history_len)
+        hist = {op: sw2d.sw2d_reduce_history(h, op, k)
+                for op in range(sw2d.SW2D_RED_N) if mask & (1 << op)}
+    finally:
+        sw2d.sw2d_destroy(h)
+    return out, hist
+
+
+def _check_history(hist, want_hist, n):
+    k = len(next(iter(hist.values())))
+    for op, series in hist.items():
+        for t in range(k):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[t]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want_hist[n - k + t, op]
+            check_reductions(row, ref)
+
+
+@pytest.mark.parametrize("kind,history_len", [("1", 300), ("2", 300), ("2", 37), ("1", 64)])
+def test_graph_replay_with_per_step_diagnostics(kind, history_len, monkeypatch):
+    """Graphs also replay with per-step diagnostics: the history slot of each
+    record is found on the device (a step counter that advances with the
+    records), so every step's record lands in its ring slot — also when the
+    ring wraps (history_len 37, 64) and chunks start on either parity."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", kind)
+    cfg, st = _bowl(300, 170)
+    n = 1 + 64 + 129 + 70
+    want = oracle_run(P, st, n, history=True)
+    got, hist = _history_run(st, [1, 64, 129, 70], ALL, history_len)
+    assert_state_equal(got, want[:4], where=f"graphs+diagnostics kind {kind}")
+    _check_history(hist, want[4], n)
+
+
+def test_graph_replay_diagnostics_virtual_ranks():
+    """Three virtual slabs (several launches per step share one record) in
+    replayed graphs with per-step diagnostics."""
+    cfg, st = _bowl(250, 120)
+    n = 2 + 64 + 66
+    want = oracle_run(P, st, n, history=True)
+    got, hist = _history_run(st, [2, 64, 66], ALL, 200,
+                             dist=sw2d.make_dist(0, 3, virtual_ranks=1))
+    assert_state_equal(got, want[:4], where="virtual ranks, graphs + diagnostics")
+    _check_history(hist, want[4], n)
