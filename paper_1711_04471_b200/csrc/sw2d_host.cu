@@ -65,6 +65,7 @@ struct sw2d {
   int64_t pitch = 0;
   int nstrips = 0;
   int red_level = 0;
+  int nstrips2 = 0;  // kind 2, two steps per launch: 56-column strips
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
   int tb_tw = 0, tb_th = 0, tb_k = 0;  // temporal blocking (small grids); tb_k = 0: off
   std::vector<Slab> slabs;
@@ -242,7 +243,7 @@ void plan_launches(sw2d* h) {
   // halo (phase 1, after the exchange); the rest (phase 0) overlap with it.
   // Virtual ranks use the same bands, so one GPU exercises the split.
   auto plan = [&](std::vector<Launch>& out, int per, long long target_segs, long long mrows,
-                  int kind) {
+                  int kind, int nstrips) {
     out.clear();
     int part = 0;
     auto add = [&](int s, long long lo, long long hi, int phase) {
@@ -257,8 +258,8 @@ void plan_launches(sw2d* h) {
       L.rows_per_seg = (int)rps;
       L.nsegs = (int)((rows + rps - 1) / rps);
       L.phase = phase;
-      L.blocks = kind == 3 ? (int)(((h->nstrips + per - 1) / per) * L.nsegs)
-                           : step_grid(kind, h->nstrips, L.nsegs);
+      L.blocks = kind == 3 ? (int)(((nstrips + per - 1) / per) * L.nsegs)
+                           : step_grid(kind, nstrips, L.nsegs);
       L.part_base = part;
       part += L.blocks;
       out.push_back(L);
@@ -277,16 +278,25 @@ void plan_launches(sw2d* h) {
     const int per = step_strips_per_cta(h->kind);
     const long long ncc = (h->nstrips + per - 1) / per;
     h->step_blocks = plan(h->launches, per, std::max(1LL, (long long)sms * bps / ncc), min_rows,
-                          h->kind);
+                          h->kind, h->nstrips);
   }
   // two steps per launch (the CTA kernel layout; one CTA per SM)
   h->launches2.clear();
   h->step_blocks2 = 0;
   const char* two_env = std::getenv("SW2D_TWO_STEP");
-  if (h->kind == 1 && h->p.variant == SW2D_VARIANT_FUSED && !(two_env && std::atoi(two_env) == 0)) {
+  const bool two = h->p.variant == SW2D_VARIANT_FUSED && !(two_env && std::atoi(two_env) == 0);
+  if (two && h->kind == 1) {
     const int per2 = step2_strips_per_cta();
     const long long ncc2 = (h->nstrips + per2 - 1) / per2;
-    h->step_blocks2 = plan(h->launches2, per2, std::max(1LL, (long long)sms / ncc2), 8, 3);
+    h->step_blocks2 = plan(h->launches2, per2, std::max(1LL, (long long)sms / ncc2), 8, 3,
+                           h->nstrips);
+  } else if (two && h->kind == 2) {  // the small-grid layout, two marches per warp
+    const int bps2 = step2_small_occupancy_blocks_per_sm(h->red_level);
+    const int per = step_strips_per_cta(2);
+    h->nstrips2 = (int)((h->p.nx + step2_small_strip_cols() - 1) / step2_small_strip_cols());
+    const long long ncc = (h->nstrips2 + per - 1) / per;
+    h->step_blocks2 = plan(h->launches2, per, std::max(1LL, (long long)sms * bps2 / ncc), 8, 2,
+                           h->nstrips2);
   }
   plan_tb(h, sms);
   {
@@ -670,7 +680,11 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
   const int64_t strips4 = (h->p.nx + kColsPerStrip - 1) / kColsPerStrip;
   h->nstrips = (int)((h->p.nx + step_strip_cols(h->kind) - 1) / step_strip_cols(h->kind));
-  const int64_t need = strips4 * kColsPerStrip + kStripBase + 8;  // covers both layouts
+  // storage columns touched: 120-column strips (kinds 0, 1; the 60-column
+  // small-grid strips fit inside) and the 56-column two-step small strips
+  const int64_t strips56 = (h->p.nx + step2_small_strip_cols() - 1) / step2_small_strip_cols();
+  const int64_t need = std::max<int64_t>(strips4 * kColsPerStrip + kStripBase + 8,
+                                         strips56 * step2_small_strip_cols() + kColOff + 5);
   h->pitch = (need + 31) / 32 * 32;
   // streams
   if (cuda_stream) {
@@ -791,6 +805,7 @@ int run_pass(sw2d* h, int spl) {
   }
   auto args = [&](const Launch& L) {
     StepArgs a = step_args(h, L, rec[0]);
+    if (spl == 2 && h->kind == 2) a.nstrips = h->nstrips2;  // 56-column two-step strips
     a.red.expected = blocks;
     a.red2 = a.red;
     a.red2.partials = h->partials + blocks;
@@ -799,7 +814,9 @@ int run_pass(sw2d* h, int spl) {
     return a;
   };
   auto launch = [&](const StepArgs& a, bool remote) {
-    if (spl == 2)
+    if (spl == 2 && h->kind == 2)
+      launch_step2_small(a, h->red_level, h->stream);
+    else if (spl == 2)
       launch_step2(a, h->red_level, h->stream, remote);
     else
       launch_step(a, h->red_level, h->kind, h->stream, remote);

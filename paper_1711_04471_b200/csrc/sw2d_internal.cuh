@@ -125,6 +125,9 @@ int step_occupancy_blocks_per_sm(int red_level, int kind);
 // Two steps per launch (kind 1 layout, one slab): state n -> n+2.
 void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote = false);
 int step2_strips_per_cta();
+void launch_step2_small(const StepArgs& a, int red_level, void* stream);  // kind 2, two steps
+int step2_small_occupancy_blocks_per_sm(int red_level);
+int step2_small_strip_cols();  // 56
 
 // set_state helper: checks finiteness of the interior, zeroes the wall faces
 // of U (k = nx) and V (global j = ny), and sums hzero in fp64 into *h0sum.

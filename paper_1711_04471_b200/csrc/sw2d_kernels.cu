@@ -819,6 +819,25 @@ struct Win2 {
 // slots updated in place (no shifting): uS / hS hold u(n+1) and hzero of the
 // row two iterations back (the caller alternates two slots), vS holds v(n+1)
 // of the row one iteration back.
+template <int RED, bool REMOTE, int C>
+__device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const float (&eL)[C],
+                                           const float (&h0L)[C], const float (&uL)[C],
+                                           const float (&vL)[C], const int L, const Ctx& x,
+                                           Acc& acc1, Acc& acc2, float* pU, float* pV, float* pE,
+                                           float (&uS)[C], float (&hS)[C], float (&vS)[C]) {
+  RowOut<C> r1;
+  row_stepC<RED, false, C, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
+                                  nullptr, &r1);
+  // state n+1 of row L-2: eta from this iteration, u from two, v from one back
+  row_stepC<RED, REMOTE, C, true>(w.s2, o.s2, r1.En, hS, uS, vS, L - 2, x, acc2, pU, pV, pE);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    uS[c] = r1.un[c];
+    hS[c] = h0L[c];
+    vS[c] = r1.vn[c];
+  }
+}
+
 template <int RED, bool REMOTE>
 __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const float4 E4,
                                           const float4 H4, const float4 U4, const float4 V4,
@@ -829,17 +848,7 @@ __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const fl
   const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
   const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
   const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
-  RowOut<4> r1;
-  row_stepC<RED, false, 4, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
-                                  nullptr, &r1);
-  // state n+1 of row L-2: eta from this iteration, u from two, v from one back
-  row_stepC<RED, REMOTE, 4, true>(w.s2, o.s2, r1.En, hS, uS, vS, L - 2, x, acc2, pU, pV, pE);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uS[c] = r1.un[c];
-    hS[c] = h0L[c];
-    vS[c] = r1.vn[c];
-  }
+  row_step2C<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vS);
 }
 
 // 7 compute warps + the producer: 8 warps (2 per scheduler) can use up to 255
@@ -1012,6 +1021,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
 constexpr int kSmallC = 2;
 constexpr int kSmallWarps = 4;
 constexpr int kSmallCols = kOutLanes * kSmallC;   // 60 output columns per strip
+constexpr int kSmall2Cols = 28 * kSmallC;         // two-step strips: 56 (2 halo lanes per side)
 
 __device__ __forceinline__ void ldg2(const float* p, float (&v)[2]) {
   const float2 t = __ldg(reinterpret_cast<const float2*>(p));
@@ -1093,6 +1103,100 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
   if (RED >= 1) block_reduce_and_finalize<RED, kSmallWarps>(acc, a.red);
 }
 
+// Two steps per launch on the small-grid layout (kind 2): each warp runs the
+// two row marches of row_step2C with C = 2 columns per lane and plain loads
+// (one row prefetched).  Two steps need a 4-column halo on each side of a
+// strip (2 per step), so lanes 0, 1 and 30, 31 are halo lanes and a strip has
+// 28 x 2 = 56 output columns.  Rows outside the stored rows read as zeros.
+template <int RED>
+__global__ void __launch_bounds__(32 * kSmallWarps)
+    sw2d_step_small2(const StepArgs a) {
+  constexpr int C = kSmallC;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kSmallWarps + (threadIdx.x >> 5);
+  const int strip = gw % a.nstrips;
+  const int seg = gw / a.nstrips;
+  Acc acc1, acc2;
+  acc1.init();
+  acc2.init();
+  if (seg < a.nsegs) {  // warp-uniform
+    Ctx x;
+    x.ra = (int)a.row_lo + seg * a.rows_per_seg;
+    x.rb = min((int)a.row_hi, x.ra + a.rows_per_seg - 1);
+    const int k0 = strip * kSmall2Cols + C * (lane - 2) + 1;  // 1-based column of element 0
+    const int c0 = k0 + kColOff;                              // its storage column
+    x.colmask = 0;
+    x.umask = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
+    }
+    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    x.q = a.c.q; x.hmin = a.c.hmin;
+    x.ny = (int)a.ny;
+    x.out_lane = (lane >= 2) && (lane <= 29);
+#ifdef SW2D_DEBUG_BOUNDS
+    x.dU = a.s.Un;
+    x.dV = a.s.Vn;
+    x.dE = a.s.En;
+    x.nelem = a.s.nelem;
+#endif
+    const long long pitch = a.s.pitch;
+    const int srows = (int)(a.s.nelem / pitch);   // storage rows of each field
+    const int first = x.ra - 4, n = x.rb + 4 - first + 1;
+    const int sfirst = first - (int)a.s.jbase;     // storage row of `first` (may be < 0)
+    const long long lo = (long long)sfirst * pitch + c0;
+    const float* __restrict__ E = a.s.E;
+    const float* __restrict__ H = a.s.H0;
+    const float* __restrict__ U = a.s.U;
+    const float* __restrict__ V = a.s.V;
+    float* __restrict__ En = a.s.En;
+    float* __restrict__ Un = a.s.Un;
+    float* __restrict__ Vn = a.s.Vn;
+    auto load = [&](int i, float (&e)[C], float (&hh)[C], float (&u)[C], float (&v)[C]) {
+      const int sr = sfirst + i;
+      if (sr < 0 || sr >= srows) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) e[c] = hh[c] = u[c] = v[c] = 0.0f;
+      } else {
+        const long long o = lo + (long long)i * pitch;
+        ldg2(E + o, e); ldg2(H + o, hh); ldg2(U + o, u); ldg2(V + o, v);
+      }
+    };
+    Win2<C> wa, wb;
+    wa.zero();
+    float uA[C] = {0.f, 0.f}, uB[C] = {0.f, 0.f}, hA[C] = {0.f, 0.f}, hB[C] = {0.f, 0.f};
+    float vS[C] = {0.f, 0.f};
+    float aE[C], aH[C], aU[C], aV[C], bE[C], bH[C], bU[C], bV[C];
+    load(0, aE, aH, aU, aV);
+    int i = 0;
+    for (; i + 1 < n; i += 2) {
+      const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
+      load(i + 1, bE, bH, bU, bV);
+      row_step2C<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc1, acc2, Un + o,
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+      if (i + 2 < n) load(i + 2, aE, aH, aU, aV);
+      row_step2C<RED, false, C>(wb, wa, bE, bH, bU, bV, first + i + 1, x, acc1, acc2,
+                                Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vS);
+    }
+    if (i < n) {
+      const long long o = lo + (long long)(i - 2) * pitch;
+      row_step2C<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc1, acc2, Un + o,
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+    }
+  }
+  if (RED >= 1) {
+    block_reduce_and_finalize<RED, kSmallWarps>(acc1, a.red);
+    block_reduce_and_finalize<RED, kSmallWarps>(acc2, a.red2);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // set_state ingest: finiteness check, wall-face zeroing, sum of hzero.
 // ---------------------------------------------------------------------------
@@ -1170,6 +1274,7 @@ int step_strips_per_cta(int kind) {
 }
 
 int step_strip_cols(int kind) { return kind == 2 ? kSmallCols : kColsPerStrip; }
+int step2_small_strip_cols() { return kSmall2Cols; }
 
 int step_grid(int kind, int nstrips, int nsegs) {
   if (kind == 2) {  // independent warps: (strip, segment) pairs, kSmallWarps per CTA
@@ -1245,6 +1350,28 @@ void launch_two(const StepArgs& a, cudaStream_t s) {
 }  // namespace
 
 int step2_strips_per_cta() { return kCta2Strips; }
+
+void launch_step2_small(const StepArgs& a, int red_level, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = step_grid(2, a.nstrips, a.nsegs);
+  if (red_level >= 2)
+    sw2d_step_small2<2><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+  else if (red_level == 1)
+    sw2d_step_small2<1><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+  else
+    sw2d_step_small2<0><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+}
+
+int step2_small_occupancy_blocks_per_sm(int red_level) {
+  int n = 0;
+  if (red_level >= 2)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<2>, 32 * kSmallWarps, 0);
+  else if (red_level == 1)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<1>, 32 * kSmallWarps, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<0>, 32 * kSmallWarps, 0);
+  return n < 1 ? 1 : n;
+}
 
 void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote) {
   cudaStream_t s = (cudaStream_t)stream;
