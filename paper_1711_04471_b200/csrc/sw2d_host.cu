@@ -88,7 +88,7 @@ struct sw2d {
   unsigned long long* dstep = nullptr;
   bool capturing = false;
   int cap_step = 0;
-  int64_t dstep_host = -1;  // value *dstep will hold when the queued work reaches it (-1: unknown)
+  RedPartial* gpart = nullptr;  // deferred partials of a captured graph's steps (small grids)
   double* hist = nullptr;
   int hist_len = 0;
   double* rec = nullptr;    // scratch record (ingest, sw2d_reduce)
@@ -553,6 +553,7 @@ void free_all(sw2d* h) {
   cudaFree(h->counter);
   cudaFree(h->dstep);
   cudaFree(h->grec);
+  cudaFree(h->gpart);
   cudaFree(h->hist);
   cudaFree(h->rec);
   cudaFree(h->h0sum);
@@ -732,6 +733,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   CUDA_TRY(h, cudaMalloc(&h->counter, 2 * sizeof(unsigned int)));
   CUDA_TRY(h, cudaMalloc(&h->dstep, sizeof(unsigned long long)));
   CUDA_TRY(h, cudaMalloc(&h->grec, sizeof(double) * kRecN * 2 * (size_t)kGraphPasses));
+  CUDA_TRY(h, cudaMalloc(&h->gpart, sizeof(RedPartial) * (size_t)cap * 2 * (size_t)kGraphPasses));
   CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, 2 * sizeof(unsigned int), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
   CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
@@ -769,7 +771,8 @@ __global__ void set_dstep(unsigned long long* dstep, unsigned long long v) { *ds
 __global__ void ring_scatter(const double* grec, double* hist, int len,
                              unsigned long long* dstep, int n) {
   const unsigned long long s0 = *dstep;
-  for (int t = threadIdx.x; t < n * kRecN; t += blockDim.x) {
+  const int first = n > len ? n - len : 0;  // earlier records would be overwritten
+  for (int t = first * kRecN + threadIdx.x; t < n * kRecN; t += blockDim.x) {
     const int i = t / kRecN, f = t % kRecN;
     hist[(size_t)((s0 + (unsigned long long)i) % (unsigned long long)len) * kRecN + f] = grec[t];
   }
@@ -787,6 +790,10 @@ int run_pass(sw2d* h, int spl) {
     rec[k] = !h->red_level ? h->rec + k * kRecN
              : h->capturing ? h->grec + (size_t)(h->cap_step + k) * kRecN
                             : h->hist + (size_t)((h->steps + k) % h->hist_len) * kRecN;
+  // captured two-step small-grid passes defer their diagnostics: CTA partials
+  // go to gpart[step within the graph], folded by fold_steps at the graph's end
+  const bool defer = h->capturing && h->red_level && spl == 2 && h->kind == 2;
+  const int cap0 = h->cap_step;
   if (h->capturing) h->cap_step += spl;
   if (h->virt && !p2p) {
     int rc = virtual_halo(h, h->cur);
@@ -811,11 +818,15 @@ int run_pass(sw2d* h, int spl) {
     a.red2.partials = h->partials + blocks;
     a.red2.counter = h->counter + 1;
     a.red2.rec = rec[1];
+    if (defer) {
+      a.red.partials = h->gpart + (size_t)cap0 * (size_t)blocks;
+      a.red2.partials = h->gpart + (size_t)(cap0 + 1) * (size_t)blocks;
+    }
     return a;
   };
   auto launch = [&](const StepArgs& a, bool remote) {
     if (spl == 2 && h->kind == 2)
-      launch_step2_small(a, h->red_level, h->stream);
+      launch_step2_small(a, h->red_level, h->stream, defer);
     else if (spl == 2)
       launch_step2(a, h->red_level, h->stream, remote);
     else
@@ -1024,7 +1035,6 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
     }
     CUDA_TRY(h, cudaGetLastError());
   }
-  h->dstep_host = -1;
   int bad = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -1114,7 +1124,10 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       h->cap_step = 0;
       for (int i = 0; i < kGraphPasses && rc == SW2D_OK; ++i) rc = run_pass(h, spl0);
       h->capturing = false;
-      if (rc == SW2D_OK && h->red_level)
+      if (rc == SW2D_OK && h->red_level && spl0 == 2 && h->kind == 2)
+        launch_fold_steps(h->gpart, h->step_blocks2, kGraphPasses * spl0, h->hist, h->hist_len,
+                          h->dstep, h->h0sum, (double)h->p.dx * (double)h->p.dy, h->stream);
+      else if (rc == SW2D_OK && h->red_level)
         ring_scatter<<<1, 256, 0, h->stream>>>(h->grec, h->hist, h->hist_len, h->dstep,
                                                kGraphPasses * spl0);
       const cudaError_t ce = cudaStreamEndCapture(h->stream, &graph);
@@ -1127,7 +1140,7 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       cudaGraphDestroy(graph);
       CUDA_TRY(h, ie);
     }
-    if (h->red_level && h->dstep_host != h->steps) {  // sync the device step counter
+    if (h->red_level) {  // the graph's first step: its history slot base
       set_dstep<<<1, 1, 0, h->stream>>>(h->dstep, (unsigned long long)h->steps);
       h->nlaunch++;
     }
@@ -1135,7 +1148,6 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
     h->nlaunch += (int64_t)kGraphPasses * (int64_t)(h->launches2.empty() ? h->launches.size()
                                                                         : h->launches2.size()) +
                   (h->red_level ? 1 : 0);
-    if (h->red_level) h->dstep_host = h->steps + (int64_t)kGraphPasses * spl0;
     h->steps += (int64_t)kGraphPasses * spl0;
     nsteps -= (int64_t)kGraphPasses * spl0;  // kGraphPasses is even: parity unchanged
   }

@@ -125,7 +125,13 @@ int step_occupancy_blocks_per_sm(int red_level, int kind);
 // Two steps per launch (kind 1 layout, one slab): state n -> n+2.
 void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote = false);
 int step2_strips_per_cta();
-void launch_step2_small(const StepArgs& a, int red_level, void* stream);  // kind 2, two steps
+void launch_step2_small(const StepArgs& a, int red_level, void* stream,
+                        bool defer = false);  // kind 2, two steps
+// fold `nsteps` steps' deferred partials (`blocks` per step) into history slots
+// (*dstep + s) % len
+void launch_fold_steps(const RedPartial* partials, int blocks, int nsteps, double* hist, int len,
+                       const unsigned long long* dstep, const double* h0sum, double dxdy,
+                       void* stream);
 int step2_small_occupancy_blocks_per_sm(int red_level);
 int step2_small_strip_cols();  // 56
 

@@ -153,6 +153,103 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
   }
 }
 
+// Deferred form (replayed graphs on small grids): the CTA's partial only; the
+// steps' records are folded later by fold_steps, off the launch's critical
+// path (no ticket, no last-CTA tail).
+template <int LEVEL, int NW>
+__device__ void block_reduce_to_partial(Acc acc, RedPartial* dst) {
+  __shared__ Acc sh[NW];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();  // sh may still be read by a previous call
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    acc.sum_eta += shfl_xor_d(acc.sum_eta, m);
+    if (LEVEL >= 2) {
+      acc.wet += shfl_xor_d(acc.wet, m);
+      acc.max_eta = fmaxf(acc.max_eta, __shfl_xor_sync(kFull, acc.max_eta, m));
+      acc.neg_min_eta = fmaxf(acc.neg_min_eta, __shfl_xor_sync(kFull, acc.neg_min_eta, m));
+      acc.max_u = fmaxf(acc.max_u, __shfl_xor_sync(kFull, acc.max_u, m));
+      acc.max_v = fmaxf(acc.max_v, __shfl_xor_sync(kFull, acc.max_v, m));
+    }
+  }
+  if (lane == 0) sh[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Acc t = sh[0];
+    for (int w = 1; w < NW; ++w) {
+      t.sum_eta += sh[w].sum_eta;
+      t.wet += sh[w].wet;
+      t.max_eta = fmaxf(t.max_eta, sh[w].max_eta);
+      t.neg_min_eta = fmaxf(t.neg_min_eta, sh[w].neg_min_eta);
+      t.max_u = fmaxf(t.max_u, sh[w].max_u);
+      t.max_v = fmaxf(t.max_v, sh[w].max_v);
+    }
+    RedPartial p;
+    p.sum_eta = t.sum_eta;
+    p.wet = t.wet;
+    p.max_eta = t.max_eta;
+    p.neg_min_eta = t.neg_min_eta;
+    p.max_u = t.max_u;
+    p.max_v = t.max_v;
+    dst[blockIdx.x] = p;
+  }
+}
+
+// CTA s folds step s's `blocks` partials (fixed order) into its record, history
+// slot (*dstep + s) % len.  The caller sets *dstep before the steps run.
+constexpr int kFoldThreads = 128;
+__global__ void __launch_bounds__(kFoldThreads)
+    fold_steps(const RedPartial* partials, int blocks, double* hist, int len,
+               const unsigned long long* dstep, const double* h0sum, double dxdy) {
+  __shared__ Acc sh[kFoldThreads / 32];
+  // a step whose slot a later step of this batch overwrites is not folded
+  // (the CTAs run in any order)
+  if ((int)blockIdx.x + len < (int)gridDim.x) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const RedPartial* p0 = partials + (size_t)blockIdx.x * blocks;
+  Acc t;
+  t.init();
+  for (int i = threadIdx.x; i < blocks; i += kFoldThreads) {
+    const RedPartial& p = p0[i];
+    t.sum_eta += p.sum_eta;
+    t.wet += p.wet;
+    t.max_eta = fmaxf(t.max_eta, p.max_eta);
+    t.neg_min_eta = fmaxf(t.neg_min_eta, p.neg_min_eta);
+    t.max_u = fmaxf(t.max_u, p.max_u);
+    t.max_v = fmaxf(t.max_v, p.max_v);
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    t.sum_eta += shfl_xor_d(t.sum_eta, m);
+    t.wet += shfl_xor_d(t.wet, m);
+    t.max_eta = fmaxf(t.max_eta, __shfl_xor_sync(kFull, t.max_eta, m));
+    t.neg_min_eta = fmaxf(t.neg_min_eta, __shfl_xor_sync(kFull, t.neg_min_eta, m));
+    t.max_u = fmaxf(t.max_u, __shfl_xor_sync(kFull, t.max_u, m));
+    t.max_v = fmaxf(t.max_v, __shfl_xor_sync(kFull, t.max_v, m));
+  }
+  if (lane == 0) sh[warp] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Acc f = sh[0];
+    for (int w = 1; w < kFoldThreads / 32; ++w) {
+      f.sum_eta += sh[w].sum_eta;
+      f.wet += sh[w].wet;
+      f.max_eta = fmaxf(f.max_eta, sh[w].max_eta);
+      f.neg_min_eta = fmaxf(f.neg_min_eta, sh[w].neg_min_eta);
+      f.max_u = fmaxf(f.max_u, sh[w].max_u);
+      f.max_v = fmaxf(f.max_v, sh[w].max_v);
+    }
+    double* rec = hist + (size_t)((*dstep + blockIdx.x) % (unsigned long long)len) * kRecN;
+    rec[kRecVol] = dxdy * (*h0sum + f.sum_eta);
+    rec[kRecSumEta] = f.sum_eta;
+    rec[kRecWet] = f.wet;
+    rec[kRecMaxEta] = f.max_eta;
+    rec[kRecNegMinEta] = f.neg_min_eta;
+    rec[kRecMaxU] = f.max_u;
+    rec[kRecMaxV] = f.max_v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The fused step.
 //
@@ -1108,8 +1205,13 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
 // (one row prefetched).  Two steps need a 4-column halo on each side of a
 // strip (2 per step), so lanes 0, 1 and 30, 31 are halo lanes and a strip has
 // 28 x 2 = 56 output columns.  Rows outside the stored rows read as zeros.
-template <int RED>
-__global__ void __launch_bounds__(32 * kSmallWarps)
+#ifndef SW2D_SMALL2_MINB
+#define SW2D_SMALL2_MINB 1
+#endif
+// DEFER: write the two steps' CTA partials to red.partials / red2.partials
+// (+ part_base + CTA) for fold_steps instead of folding them here.
+template <int RED, bool DEFER>
+__global__ void __launch_bounds__(32 * kSmallWarps, SW2D_SMALL2_MINB)
     sw2d_step_small2(const StepArgs a) {
   constexpr int C = kSmallC;
   const int lane = threadIdx.x & 31;
@@ -1191,7 +1293,10 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
                                 Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
     }
   }
-  if (RED >= 1) {
+  if (RED >= 1 && DEFER) {
+    block_reduce_to_partial<RED, kSmallWarps>(acc1, a.red.partials + a.red.part_base);
+    block_reduce_to_partial<RED, kSmallWarps>(acc2, a.red2.partials + a.red2.part_base);
+  } else if (RED >= 1) {
     block_reduce_and_finalize<RED, kSmallWarps>(acc1, a.red);
     block_reduce_and_finalize<RED, kSmallWarps>(acc2, a.red2);
   }
@@ -1351,25 +1456,36 @@ void launch_two(const StepArgs& a, cudaStream_t s) {
 
 int step2_strips_per_cta() { return kCta2Strips; }
 
-void launch_step2_small(const StepArgs& a, int red_level, void* stream) {
+void launch_step2_small(const StepArgs& a, int red_level, void* stream, bool defer) {
   cudaStream_t s = (cudaStream_t)stream;
   const int blocks = step_grid(2, a.nstrips, a.nsegs);
-  if (red_level >= 2)
-    sw2d_step_small2<2><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+  if (red_level >= 2 && defer)
+    sw2d_step_small2<2, true><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+  else if (red_level >= 2)
+    sw2d_step_small2<2, false><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+  else if (red_level == 1 && defer)
+    sw2d_step_small2<1, true><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
   else if (red_level == 1)
-    sw2d_step_small2<1><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+    sw2d_step_small2<1, false><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
   else
-    sw2d_step_small2<0><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+    sw2d_step_small2<0, false><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
+}
+
+void launch_fold_steps(const RedPartial* partials, int blocks, int nsteps, double* hist, int len,
+                       const unsigned long long* dstep, const double* h0sum, double dxdy,
+                       void* stream) {
+  fold_steps<<<nsteps, kFoldThreads, 0, (cudaStream_t)stream>>>(partials, blocks, hist, len,
+                                                               dstep, h0sum, dxdy);
 }
 
 int step2_small_occupancy_blocks_per_sm(int red_level) {
   int n = 0;
   if (red_level >= 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<2>, 32 * kSmallWarps, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<2, false>, 32 * kSmallWarps, 0);
   else if (red_level == 1)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<1>, 32 * kSmallWarps, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<1, false>, 32 * kSmallWarps, 0);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<0>, 32 * kSmallWarps, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small2<0, false>, 32 * kSmallWarps, 0);
   return n < 1 ? 1 : n;
 }
 
