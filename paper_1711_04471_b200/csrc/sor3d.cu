@@ -407,7 +407,6 @@ struct sor3d {
   int cap = 0;
   int rows_cta = 32;  // extended tile rows (CTA = 16 x rows_cta threads)
   bool hint = false;  // L2 eviction hints (p and rhs fit in L2)
-  size_t persist_bytes = 0;  // L2 persisting window over rhs (0: none)
   int64_t nrec = 0;
   bool have_state = false;
   int64_t nlaunch = 0;
@@ -495,17 +494,6 @@ int launch(sor3d* h, bool write, double* rec) {
   cfg.gridDim = dim3((unsigned)h->gx, (unsigned)h->gy, (unsigned)h->gz);
   cfg.blockDim = dim3(kSx * h->rows_cta);
   cfg.stream = h->stream;
-  cudaLaunchAttribute attr[1];
-  if (h->persist_bytes > 0) {  // rhs persists in L2 (SOR3D_PERSIST)
-    attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[0].val.accessPolicyWindow.base_ptr = h->rhs;
-    attr[0].val.accessPolicyWindow.num_bytes = h->persist_bytes;
-    attr[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-  }
   SOR_TRY(h, cudaLaunchKernelEx(&cfg, k, a));
   ++h->nlaunch;
   SOR_TRY(h, cudaGetLastError());
@@ -686,17 +674,6 @@ int sor3d_create(const sor3d_params* prm, void* cuda_stream, sor3d** out) {
   for (float** f : {&h->p[0], &h->p[1], &h->rhs}) {
     CREATE_TRY(cudaMalloc(f, bytes));
     CREATE_TRY(cudaMemset(*f, 0, bytes));
-  }
-  if (const char* e = std::getenv("SOR3D_PERSIST")) {
-    if (std::atoi(e) != 0) {
-      int maxp = 0, maxw = 0;
-      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-      cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, h->device);
-      h->persist_bytes = std::min({bytes, (size_t)maxp, (size_t)maxw});
-      if (h->persist_bytes) CREATE_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, h->persist_bytes));
-      std::fprintf(stderr, "sor3d: persisting L2 window %zu bytes (max persist %d, max window %d)\n",
-                   h->persist_bytes, maxp, maxw);
-    }
   }
   const int nparts = h->gx * h->gy * h->gz;
   h->cap = prm->history_len > 0 ? prm->history_len : 1024;
