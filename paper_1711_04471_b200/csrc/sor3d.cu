@@ -201,7 +201,12 @@ struct March {
   float4 pz0, pz1, pz2, pf;
   float4 r1, r2, rf1, rf2;
   float4 n0, n1;
-  const float* pp;  // p_in plane m+3 (next prefetch)
+  // the three streams: without the residual, one 32-bit element offset of
+  // this lane's quad in plane m+3 (p_in and rhs; p_out plane m-1 is ofs - 4
+  // planes; sor3d_create keeps arrays below 2^31 elements); with it, three
+  // pointers (each form measured best for its variant)
+  unsigned ofs;
+  const float* pp;  // p_in plane m+3
   const float* rp;  // rhs plane m+3
   float* op;        // p_out plane m-1
   double acc;
@@ -222,6 +227,8 @@ struct Lane {
   long long plane;
   int intr;      // bit c: cell c is an interior cell (the red update applies)
   int outm;      // bit c: cell c is an output cell (tile, interior): stored
+  bool all4;     // outm == 15
+  bool anyout;   // outm != 0
   int tx, ty;
   int yn, ys;
 };
@@ -280,12 +287,23 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
         const float ns = nsum(E, W, compv(Nb, c), compv(Sb, c), compv(pn, c), compv(st.n0, c), a);
         comp(o, c) = upd(compv(st.n1, c), ns, compv(st.r1, c), a);
       }
-      if (L.outm == 15) {
-        sth<H>(st.op, o);
-      } else if (L.outm) {
+      if constexpr (RES) {
+        if (L.outm == 15) {
+          sth<H>(st.op, o);
+        } else if (L.outm) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (L.outm >> c & 1) st.op[c] = compv(o, c);
+          for (int c = 0; c < 4; ++c)
+            if (L.outm >> c & 1) st.op[c] = compv(o, c);
+        }
+      } else {
+        float* op = a.pout + (st.ofs - 4u * (unsigned)L.plane);
+        if (L.all4) {
+          sth<H>(op, o);
+        } else if (L.anyout) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (L.outm >> c & 1) op[c] = compv(o, c);
+        }
       }
     }
   }
@@ -293,16 +311,20 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
   st.pz0 = st.pz1;
   st.pz1 = st.pz2;
   st.pz2 = st.pf;
-  st.pf = ldh<H, false>(st.pp);
+  st.pf = ldh<H, false>(RES ? st.pp : a.pin + st.ofs);
   st.r1 = st.r2;
   st.r2 = st.rf1;
   st.rf1 = st.rf2;
-  st.rf2 = ldh<H, true>(st.rp);
+  st.rf2 = ldh<H, true>(RES ? st.rp : a.rhs + st.ofs);
   st.n0 = st.n1;
   st.n1 = pn;
-  st.pp += L.plane;
-  st.rp += L.plane;
-  st.op += L.plane;
+  if constexpr (RES) {
+    st.pp += L.plane;
+    st.rp += L.plane;
+    st.op += L.plane;
+  } else {
+    st.ofs += (unsigned)L.plane;
+  }
 }
 
 template <int R, int P0, bool RES, bool WRITE, bool H>
@@ -349,6 +371,8 @@ __global__ void __launch_bounds__(kSx * R, SOR_MINB(R)) sor_iter(const Args a) {
     if (in) L.intr |= 1 << c;
     if (in && outy && x >= 2 && x <= 4 * kSx - 3) L.outm |= 1 << c;
   }
+  L.all4 = L.outm == 15;
+  L.anyout = L.outm != 0;
   L.tx = tx;
   L.ty = ty;
   L.yn = min(ty + 1, R - 1);
@@ -367,9 +391,13 @@ __global__ void __launch_bounds__(kSx * R, SOR_MINB(R)) sor_iter(const Args a) {
   st.rf2 = ldh<H, true>(a.rhs + at(L.k0 + 1));
   st.n0 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   st.n1 = st.n0;
-  st.pp = a.pin + at(L.k0 + 2);
-  st.rp = a.rhs + at(L.k0 + 2);
-  st.op = a.pout + at(L.k0 - 2);
+  if constexpr (RES) {
+    st.pp = a.pin + at(L.k0 + 2);
+    st.rp = a.rhs + at(L.k0 + 2);
+    st.op = a.pout + at(L.k0 - 2);
+  } else {
+    st.ofs = (unsigned)at(L.k0 + 2);
+  }
   st.acc = 0.0;
   st.amx = 0.0f;
   const int nsteps = L.k1 - L.k0 + 3;  // m = k0-1 .. k1+1 (rounded up to 4: extra steps store nothing)
@@ -660,6 +688,10 @@ int sor3d_create(const sor3d_params* prm, void* cuda_stream, sor3d** out) {
   h->rows = (long long)h->gy * outy + 4;
   h->planes = (long long)h->gz * h->kz + 12;
   h->plane = h->pitch * h->rows;
+  if (h->plane * h->planes >= (1LL << 31)) {  // 32-bit element offsets in the kernel
+    h->err = "grid too large (padded arrays must stay below 2^31 elements)";
+    return bail(SOR3D_EINVAL);
+  }
   const size_t bytes = (size_t)h->plane * (size_t)h->planes * sizeof(float);
   int l2 = 0;
   cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->device);
