@@ -217,3 +217,12 @@ def test_cta_rows_variants(rows, monkeypatch):
     assert f"64x{rows}" in plan
     assert_bitwise(got, want, f"rows={rows}")
     check_hist(gh, wh)
+
+
+def test_create_rejects_grids_beyond_32bit_offsets():
+    """The kernel addresses its streams with 32-bit element offsets: padded
+    arrays of 2^31 elements or more are refused before any allocation."""
+    with pytest.raises(sor3d.Sor3dError) as ei:
+        sor3d.sor3d_create(sor3d.make_params(2048, 2048, 2048))
+    assert ei.value.code == sor3d.SOR3D_EINVAL
+    assert "2^31" in str(ei.value)
