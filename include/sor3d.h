@@ -68,7 +68,9 @@ int sor3d_abi_version(void);
 /* Create a handle on the current device.  cuda_stream: a cudaStream_t to
  * enqueue on, or NULL for a library-owned stream.  Allocates two pressure
  * buffers (ping-pong) and rhs, each padded (DESIGN.md §13 "Layout").
- * *out = NULL on failure. */
+ * SOR3D_EINVAL also if a padded array would reach 2^31 elements (about
+ * 1.9e9 cells: the kernel uses 32-bit element offsets).  *out = NULL on
+ * failure. */
 int sor3d_create(const sor3d_params* params, void* cuda_stream, sor3d** out);
 
 /* Upload p (initial guess; NULL = 0) and rhs, [nz][ny][nx] float32.
