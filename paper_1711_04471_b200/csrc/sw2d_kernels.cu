@@ -921,7 +921,8 @@ __device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const f
                                            const float (&h0L)[C], const float (&uL)[C],
                                            const float (&vL)[C], const int L, const Ctx& x,
                                            Acc& acc1, Acc& acc2, float* pU, float* pV, float* pE,
-                                           float (&uS)[C], float (&hS)[C], float (&vS)[C]) {
+                                           float (&uS)[C], float (&hS)[C], const float (&vS)[C],
+                                           float (&vOut)[C]) {
   RowOut<C> r1;
   row_stepC<RED, false, C, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
                                   nullptr, &r1);
@@ -931,7 +932,7 @@ __device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const f
   for (int c = 0; c < C; ++c) {
     uS[c] = r1.un[c];
     hS[c] = h0L[c];
-    vS[c] = r1.vn[c];
+    vOut[c] = r1.vn[c];
   }
 }
 
@@ -940,12 +941,14 @@ __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const fl
                                           const float4 H4, const float4 U4, const float4 V4,
                                           const int L, const Ctx& x, Acc& acc1, Acc& acc2,
                                           float* pU, float* pV, float* pE, float (&uS)[4],
-                                          float (&hS)[4], float (&vS)[4]) {
+                                          float (&hS)[4], const float (&vS)[4],
+                                          float (&vOut)[4]) {
   const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
   const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
   const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
   const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
-  row_step2C<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vS);
+  row_step2C<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vS,
+                             vOut);
 }
 
 // 7 compute warps + the producer: 8 warps (2 per scheduler) can use up to 255
@@ -1055,7 +1058,8 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
     wa.zero();
     float uA[4] = {0.f, 0.f, 0.f, 0.f}, uB[4] = {0.f, 0.f, 0.f, 0.f};
     float hA[4] = {0.f, 0.f, 0.f, 0.f}, hB[4] = {0.f, 0.f, 0.f, 0.f};
-    float vS[4] = {0.f, 0.f, 0.f, 0.f};
+    // v(n+1) of the row one iteration back, alternating slots (no copies)
+    float vA[4] = {0.f, 0.f, 0.f, 0.f}, vB[4] = {0.f, 0.f, 0.f, 0.f};
     float* __restrict__ En = a.s.En;
     float* __restrict__ Un = a.s.Un;
     float* __restrict__ Vn = a.s.Vn;
@@ -1087,17 +1091,17 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
       fetch(i, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
       fetch(i + 1, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
-                     Vn + o, En + o - pitch, uB, hB, vS);
+                     Vn + o, En + o - pitch, uB, hB, vA, vB);
     }
     if (i < n) {
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)(i - 2) * pitch;
       fetch(i, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
     }
   }
   if (RED >= 1) {
@@ -1274,7 +1278,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, SW2D_SMALL2_MINB)
     Win2<C> wa, wb;
     wa.zero();
     float uA[C] = {0.f, 0.f}, uB[C] = {0.f, 0.f}, hA[C] = {0.f, 0.f}, hB[C] = {0.f, 0.f};
-    float vS[C] = {0.f, 0.f};
+    float vA[C] = {0.f, 0.f}, vB[C] = {0.f, 0.f};
     float aE[C], aH[C], aU[C], aV[C], bE[C], bH[C], bU[C], bV[C];
     load(0, aE, aH, aU, aV);
     int i = 0;
@@ -1282,15 +1286,15 @@ __global__ void __launch_bounds__(32 * kSmallWarps, SW2D_SMALL2_MINB)
       const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
       load(i + 1, bE, bH, bU, bV);
       row_step2C<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc1, acc2, Un + o,
-                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
       if (i + 2 < n) load(i + 2, aE, aH, aU, aV);
       row_step2C<RED, false, C>(wb, wa, bE, bH, bU, bV, first + i + 1, x, acc1, acc2,
-                                Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vS);
+                                Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vA, vB);
     }
     if (i < n) {
       const long long o = lo + (long long)(i - 2) * pitch;
       row_step2C<RED, false, C>(wa, wb, aE, aH, aU, aV, first + i, x, acc1, acc2, Un + o,
-                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vS);
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
     }
   }
   if (RED >= 1 && DEFER) {
