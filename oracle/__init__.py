@@ -1,17 +1,24 @@
 """oracle — TEST INFRASTRUCTURE ONLY: the CPU parity oracles of the 2DSW step
 and (NEXT-4) of red-black SOR for the Poisson equation.
 
-Plain single-threaded C11 (``oracle/sw2d_ref.c``), loaded with ctypes.  It
-follows arXiv 1711.04471 §6.2 (time loop -> predictor
-``dyn`` -> first-order Shapiro filter ``shapiro`` -> velocity update) with the
-textbook scheme and readings listed in DESIGN.md.
+Plain single-threaded C11 (``oracle/sw2d_ref.c``, ``oracle/sor_ref.c``),
+loaded with ctypes.  The 2DSW oracle follows arXiv 1711.04471 §6.2
+(time loop -> predictor ``dyn`` -> first-order Shapiro
+filter ``shapiro`` -> velocity update) with the textbook scheme and readings
+listed in DESIGN.md §3; the SOR oracle follows the UFLES
+``press`` solver of §6.3 with the readings
+S1-S9 of DESIGN.md §13.
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
 ``cpu_baseline`` / ``--impl reference`` leg may import this package.  It shares
 no code with ``paper_1711_04471_b200`` and never imports it.
 
-Parity unpinned by the paper: the blocked-face velocity rule (reading R4) and
-the operation order (R12); they are pinned only by the DESIGN.md readings.
+Pins: ``tests/test_oracle_pins.py`` (2DSW: invariants, closed forms, hand
+examples) and ``tests/test_sor_oracle_pins.py`` (SOR: hand example, dense
+solve, O(h^2) manufactured solution, exact polynomial residual, Gauss-Seidel
+property).  Parity unpinned by the paper: the 2DSW blocked-face velocity rule
+(reading R4) and operation order (R12), and the SOR operation order (S4);
+they are pinned only by the DESIGN.md readings.
 """
 from __future__ import annotations
 

@@ -131,3 +131,17 @@ def test_red_black_gauss_seidel_property():
     black = (kk + jj + ii) % 2 == 1
     assert np.max(np.abs(r[black])) < 1e-5
     assert np.max(np.abs(r[~black])) > 1e-2
+
+
+def test_sor_inputs_are_pure_functions_of_index():
+    """The shared input generator (no method arithmetic): any plane range
+    equals the same planes of the full generation (so any slab can be made on
+    its own), and the paper-shaped config has the stated shape."""
+    import sor_inputs as so
+    cfg = so.config("sor_s2")
+    p0, rhs = so.generate(cfg)
+    p1, r1 = so.generate(cfg, k0=13, nk=9)
+    assert np.array_equal(p0[13:22], p1) and np.array_equal(rhs[13:22], r1)
+    c = so.config("sor300")
+    assert (c["nx"], c["ny"], c["nz"], c["iters"]) == (300, 300, 90, 50)
+    assert np.all(np.isfinite(rhs)) and np.abs(p0).max() <= 0.01
