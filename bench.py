@@ -174,6 +174,37 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_info():
+    """Host CPU model and core count (the oracle runs on one of them)."""
+    model = platform.processor() or platform.machine()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu": model, "of_cores": os.cpu_count()}
+
+
+class OneCore:
+    """Pin this process to one core while the single-threaded oracle runs."""
+
+    def __enter__(self):
+        self.saved = None
+        try:
+            self.saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(self.saved)})
+        except (AttributeError, OSError):
+            self.saved = None
+        return self
+
+    def __exit__(self, *a):
+        if self.saved is not None:
+            os.sched_setaffinity(0, self.saved)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -212,13 +243,14 @@ def run_reference(args, cfg, ws, rank):
         return
     import oracle
     params, st, steps, cells, desc = oracle_sample(cfg)
-    for _ in range(max(args.warmup, 0)):
-        oracle.run(params, *st, steps)
     times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        oracle.run(params, *st, steps)
-        times.append(time.perf_counter() - t)
+    with OneCore():
+        for _ in range(max(args.warmup, 0)):
+            oracle.run(params, *st, steps)
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            oracle.run(params, *st, steps)
+            times.append(time.perf_counter() - t)
     tot = sum(times)
     value = cells * steps * args.steps / tot
     line = {
@@ -227,8 +259,8 @@ def run_reference(args, cfg, ws, rank):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(cfg, args, ws),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": desc, "cpu": platform.processor() or platform.machine()},
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                              "sample": desc}, **cpu_info()),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -424,11 +456,12 @@ def run_ours(args, cfg, ws, rank, local):
     if ws == 1 and not args.no_cpu_baseline and not args.profile:
         import oracle
         params, st, steps, cells, desc = oracle_sample(cfg)
-        t = time.perf_counter()
-        oracle.run(params, *st, steps)
-        dt_s = time.perf_counter() - t
-        cpu = {"value": cells * steps / dt_s, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": desc, "seconds": dt_s}
+        with OneCore():
+            t = time.perf_counter()
+            oracle.run(params, *st, steps)
+            dt_s = time.perf_counter() - t
+        cpu = dict({"value": cells * steps / dt_s, "unit": UNIT, "cores": 1, "kind": "oracle",
+                    "sample": desc, "seconds": dt_s}, **cpu_info())
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
@@ -475,13 +508,14 @@ def run_sor_reference(args, cfg, rank):
     prm = so.params()
     n = min(args.sor_iters or cfg["iters"], 10)
     hist = args.sor_residual_every > 0
-    for _ in range(max(args.warmup, 0)):
-        oracle.sor_run(prm, p0, rhs, 1, history=hist)
     times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        oracle.sor_run(prm, p0, rhs, n, history=hist)
-        times.append(time.perf_counter() - t)
+    with OneCore():
+        for _ in range(max(args.warmup, 0)):
+            oracle.sor_run(prm, p0, rhs, 1, history=hist)
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            oracle.sor_run(prm, p0, rhs, n, history=hist)
+            times.append(time.perf_counter() - t)
     tot = sum(times)
     cells = so.cells(cfg)
     value = cells * n * args.steps / tot
@@ -493,8 +527,8 @@ def run_sor_reference(args, cfg, rank):
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": sor_config(cfg, args, n, args.sor_residual_every),
-        "cpu_baseline": {"value": value, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
-                         "sample": desc},
+        "cpu_baseline": dict({"value": value, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
+                              "sample": desc}, **cpu_info()),
         "e2e": {"value": value, "unit": SOR_UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -606,12 +640,14 @@ def run_sor_ours(args, cfg, ws, rank, local):
     if ws == 1 and not args.no_cpu_baseline and not args.profile:
         import oracle
         ns = 10
-        t = time.perf_counter()
-        oracle.sor_run(so.params(), p0, rhs, ns, history=every > 0)
-        dt_s = time.perf_counter() - t
-        cpu = {"value": cells * ns / dt_s, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"the full grid, {ns} iterations (residual every iteration: "
-                         f"{every > 0}), single-threaded C oracle", "seconds": dt_s}
+        with OneCore():
+            t = time.perf_counter()
+            oracle.sor_run(so.params(), p0, rhs, ns, history=every > 0)
+            dt_s = time.perf_counter() - t
+        cpu = dict({"value": cells * ns / dt_s, "unit": SOR_UNIT, "cores": 1, "kind": "oracle",
+                    "sample": f"the full grid, {ns} iterations (residual every iteration: "
+                              f"{every > 0}), single-threaded C oracle", "seconds": dt_s},
+                   **cpu_info())
     print(json.dumps({
         "metric": SOR_METRIC, "value": value, "unit": SOR_UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
