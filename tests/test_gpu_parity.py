@@ -430,14 +430,16 @@ def test_snapshots_equal_oracle_states(dist):
 
 # --- kernel variants forced on oracle-sized grids --------------------------
 
-@pytest.mark.parametrize("kind,two", [("1", "1"), ("1", "0"), ("0", "0"), ("2", "0")])
-@pytest.mark.parametrize("nx,ny,n", [(517, 389, 41), (241, 600, 30), (120, 121, 7), (9, 13, 5)])
+@pytest.mark.parametrize("kind,two", [("1", "1"), ("1", "0"), ("0", "0"), ("2", "1"), ("2", "0")])
+@pytest.mark.parametrize("nx,ny,n", [(517, 389, 41), (241, 600, 30), (120, 121, 7), (9, 13, 5),
+                                     (57, 70, 9), (113, 33, 12)])
 def test_kernel_kinds_bitwise(kind, two, nx, ny, n, monkeypatch):
     """Every step-kernel kind on the same grids (the size heuristic picks
     only one of them per grid): the CTA/TMA kernel with two steps per launch
     (and an odd step count), one step per launch, the per-warp ring, and the
-    small-grid kernel — all bitwise equal to the oracle, with all fused
-    per-step diagnostics."""
+    small-grid kernels with two steps (56-column strips: 57 and 113 columns
+    end one column into a strip) and one step per launch — all bitwise equal
+    to the oracle, with all fused per-step diagnostics."""
     monkeypatch.setenv("SW2D_STEP_KERNEL", kind)
     monkeypatch.setenv("SW2D_TWO_STEP", two)
     st = _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny)
