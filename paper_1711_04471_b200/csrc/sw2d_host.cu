@@ -295,7 +295,9 @@ void plan_launches(sw2d* h) {
     const int per = step_strips_per_cta(2);
     h->nstrips2 = (int)((h->p.nx + step2_small_strip_cols() - 1) / step2_small_strip_cols());
     const long long ncc = (h->nstrips2 + per - 1) / per;
-    h->step_blocks2 = plan(h->launches2, per, std::max(1LL, (long long)sms * bps2 / ncc), 8, 2,
+    long long mrows2 = 2;  // min output rows per two-step segment (it streams 8 more; measured)
+    if (const char* e = std::getenv("SW2D_MIN_ROWS2")) mrows2 = std::max(1, std::atoi(e));
+    h->step_blocks2 = plan(h->launches2, per, std::max(1LL, (long long)sms * bps2 / ncc), mrows2, 2,
                            h->nstrips2);
   }
   plan_tb(h, sms);
