@@ -66,6 +66,7 @@ struct sw2d {
   int nstrips = 0;
   int red_level = 0;
   int nstrips2 = 0;  // kind 2, two steps per launch: 56-column strips
+  int64_t fault_skip_halo = -1;  // SW2D_FAULT_SKIP_HALO (tests only)
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
   int tb_tw = 0, tb_th = 0, tb_k = 0;  // temporal blocking (small grids); tb_k = 0: off
   std::vector<Slab> slabs;
@@ -681,6 +682,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     h->kind = (v == 0 || v == 2) ? v : 1;
   }
   if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
+  if (const char* e = std::getenv("SW2D_FAULT_SKIP_HALO")) h->fault_skip_halo = std::atoll(e);
   const int64_t strips4 = (h->p.nx + kColsPerStrip - 1) / kColsPerStrip;
   h->nstrips = (int)((h->p.nx + step_strip_cols(h->kind) - 1) / step_strip_cols(h->kind));
   // storage columns touched: 120-column strips (kinds 0, 1; the 60-column
@@ -797,7 +799,11 @@ int run_pass(sw2d* h, int spl) {
   const bool defer = h->capturing && h->red_level && spl == 2 && h->kind == 2;
   const int cap0 = h->cap_step;
   if (h->capturing) h->cap_step += spl;
-  if (h->virt && !p2p) {
+  // fault injection (tests of the tests): SW2D_FAULT_SKIP_HALO=k drops the
+  // halo exchange of the pass that starts step k
+  const bool skip_halo = h->fault_skip_halo >= 0 && h->fault_skip_halo >= h->steps &&
+                         h->fault_skip_halo < h->steps + spl;
+  if (h->virt && !p2p && !skip_halo) {
     int rc = virtual_halo(h, h->cur);
     if (rc) return rc;
   }

@@ -550,3 +550,40 @@ def test_graph_replay_diagnostics_virtual_ranks():
                              dist=sw2d.make_dist(0, 3, virtual_ranks=1))
     assert_state_equal(got, want[:4], where="virtual ranks, graphs + diagnostics")
     _check_history(hist, want[4], n)
+
+
+# --- tests of the tests: fault injection and mapping permutation -------------
+
+def test_fault_injection_skipped_halo_fails_parity(monkeypatch):
+    """SW2D_FAULT_SKIP_HALO drops one halo exchange between virtual slabs: the
+    parity check must catch it (it would pass a checker that compares a slab
+    only with itself)."""
+    cfg, st = _bowl(240, 96)
+    n = 12
+    want = oracle_run(P, st, n)
+    dist = sw2d.make_dist(0, 3, virtual_ranks=1)
+    got, _, _, _ = gpu_run(P, st, n, dist=dist)
+    assert_state_equal(got, want, where="no fault")
+    monkeypatch.setenv("SW2D_FAULT_SKIP_HALO", "4")
+    monkeypatch.setenv("SW2D_GRAPHS", "0")
+    bad, _, _, _ = gpu_run(P, st, n, dist=dist)
+    with pytest.raises(AssertionError):
+        assert_state_equal(bad, want, where="skipped halo at step 4")
+
+
+@pytest.mark.parametrize("env", [dict(SW2D_STEP_KERNEL="1", SW2D_MIN_ROWS="1"),
+                                 dict(SW2D_STEP_KERNEL="1", SW2D_CTAS_PER_SM="1"),
+                                 dict(SW2D_STEP_KERNEL="1", SW2D_MIN_ROWS="64"),
+                                 dict(SW2D_STEP_KERNEL="2", SW2D_MIN_ROWS2="1"),
+                                 dict(SW2D_STEP_KERNEL="2", SW2D_MIN_ROWS2="40"),
+                                 dict(SW2D_STEP_KERNEL="1", SW2D_GRAPHS="0")])
+def test_mapping_permutations_bitwise(env, monkeypatch):
+    """Map soundness (SPEC's permutation check, adapted): other segmentations
+    of the grid into CTAs/warps, and graphs off, give bitwise the same
+    fields — every cell's arithmetic is independent of the mapping."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg, st = _bowl(700, 300)
+    want = oracle_run(P, st, 66)
+    got, _, _, _ = gpu_run(P, st, 66)
+    assert_state_equal(got, want, where=str(env))
