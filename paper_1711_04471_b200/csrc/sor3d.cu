@@ -43,6 +43,7 @@
 #include <string>
 
 #include "sor3d.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace sor3d_dev {
 
@@ -446,6 +447,11 @@ namespace {
 
 thread_local std::string t_create_err;
 
+struct NvtxRange {  // NVTX range over an API call
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 int fail(sor3d* h, int code, const std::string& msg) {
   if (h) {
     h->err = msg;
@@ -727,6 +733,7 @@ int sor3d_create(const sor3d_params* prm, void* cuda_stream, sor3d** out) {
 }
 
 int sor3d_set(sor3d* h, const float* p, const float* rhs) {
+  NvtxRange nvtx_("sor3d_set");
   SOR_ENTER(h);
   if (!rhs) return fail(h, SOR3D_EINVAL, "rhs is NULL");
   h->have_state = false;
@@ -752,6 +759,7 @@ int sor3d_set(sor3d* h, const float* p, const float* rhs) {
 }
 
 int sor3d_iterate(sor3d* h, int64_t n, int64_t every) {
+  NvtxRange nvtx_("sor3d_iterate");
   SOR_ENTER(h);
   if (n < 0 || every < 0) return fail(h, SOR3D_EINVAL, "n and residual_every must be >= 0");
   if (!h->have_state) return fail(h, SOR3D_ESTATE, "sor3d_iterate before sor3d_set");
@@ -769,6 +777,7 @@ int sor3d_iterate(sor3d* h, int64_t n, int64_t every) {
 }
 
 int sor3d_residual(sor3d* h, double out[2]) {
+  NvtxRange nvtx_("sor3d_residual");
   SOR_ENTER(h);
   if (!out) return fail(h, SOR3D_EINVAL, "out is NULL");
   if (!h->have_state) return fail(h, SOR3D_ESTATE, "sor3d_residual before sor3d_set");
@@ -794,6 +803,7 @@ int sor3d_residual_history(sor3d* h, double* out, int64_t n) {
 int64_t sor3d_history_count(const sor3d* h) { return h ? h->nrec : -1; }
 
 int sor3d_get(sor3d* h, float* p) {
+  NvtxRange nvtx_("sor3d_get");
   SOR_ENTER(h);
   if (!p) return fail(h, SOR3D_EINVAL, "p is NULL");
   if (!h->have_state) return fail(h, SOR3D_ESTATE, "sor3d_get before sor3d_set");

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "sw2d.h"
+#include <nvtx3/nvToolsExt.h>
 #include "sw2d_internal.cuh"
 #include "sw2d_nccl.cuh"
 
@@ -130,6 +131,13 @@ struct sw2d {
 };
 
 namespace {
+
+// NVTX range over an API call (visible in nsys / ncu timelines; ~free
+// without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(sw2d* h, int code, const std::string& msg) {
   if (h) {
@@ -967,6 +975,7 @@ int sw2d_local_rows(const sw2d* h, int64_t* j0, int64_t* nrows) {
 
 int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
                    const float* u, const float* v) {
+  NvtxRange nvtx_("sw2d_set_state");
   ENTER(h);
   if (!hzero || !eta) return fail(h, SW2D_EINVAL, "hzero and eta are required");
   const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
@@ -1057,6 +1066,7 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
 }
 
 int sw2d_step(sw2d* h, int64_t nsteps) {
+  NvtxRange nvtx_("sw2d_step");
   ENTER(h);
   if (nsteps < 0) return fail(h, SW2D_EINVAL, "nsteps must be >= 0");
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_step before sw2d_set_state");
@@ -1183,6 +1193,7 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
 
 int sw2d_run_snapshots(sw2d* h, int64_t nsteps, int64_t every, float* out_eta,
                        int64_t nsnap) {
+  NvtxRange nvtx_("sw2d_run_snapshots");
   ENTER(h);
   if (!out_eta || every < 1 || nsteps < 0 || nsnap != nsteps / every)
     return fail(h, SW2D_EINVAL, "need every >= 1, nsnap == nsteps / every, out_eta");
@@ -1247,6 +1258,7 @@ int sw2d_sync(sw2d* h) {
 }
 
 int sw2d_reduce(sw2d* h, int op, double* out) {
+  NvtxRange nvtx_("sw2d_reduce");
   ENTER(h);
   if (!out || op < 0 || op >= SW2D_RED_N) return fail(h, SW2D_EINVAL, "bad op / out");
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_reduce before sw2d_set_state");
@@ -1266,6 +1278,7 @@ int sw2d_reduce(sw2d* h, int op, double* out) {
 }
 
 int sw2d_reduce_history(sw2d* h, int op, double* out, int64_t n) {
+  NvtxRange nvtx_("sw2d_reduce_history");
   ENTER(h);
   if (!out || op < 0 || op >= SW2D_RED_N || n < 0)
     return fail(h, SW2D_EINVAL, "bad op / out / n");
@@ -1286,6 +1299,7 @@ int sw2d_reduce_history(sw2d* h, int op, double* out, int64_t n) {
 }
 
 int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
+  NvtxRange nvtx_("sw2d_get_state");
   ENTER(h);
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_get_state before sw2d_set_state");
   const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
