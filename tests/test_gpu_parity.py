@@ -587,3 +587,28 @@ def test_mapping_permutations_bitwise(env, monkeypatch):
     want = oracle_run(P, st, 66)
     got, _, _, _ = gpu_run(P, st, 66)
     assert_state_equal(got, want, where=str(env))
+
+
+@pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
+def test_single_rank_nccl_machinery(halo, monkeypatch):
+    """One real rank with the NCCL path forced on (SW2D_FORCE_NCCL): the
+    library's NCCL communicator, comm stream, grouped halo exchange (no
+    peers), per-step diagnostics allreduces and, in P2P mode, the IPC-handle
+    all-gather all run on the GPU; fields stay bitwise and every per-step
+    record equals the oracle's.  (Two real ranks need two GPUs.)"""
+    monkeypatch.setenv("SW2D_FORCE_NCCL", "1")
+    cfg, st = _bowl(300, 200)
+    n = 23
+    want = oracle_run(P, st, n, history=True)
+    uid = sw2d.sw2d_nccl_unique_id()
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL,
+                                dist=sw2d.make_dist(0, 1, 0, 0, uid, halo))
+    assert_state_equal(got, want[:4], where=f"forced NCCL, halo {halo}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    for op, series in hist.items():
+        for k in range(n):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[k]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want[4][k, op]
+            check_reductions(row, ref)
