@@ -455,7 +455,7 @@ def run_ours(args, cfg, ws, rank, local):
     cpu = None
     if ws == 1 and not args.no_cpu_baseline and not args.profile:
         import oracle
-        params, st, steps, cells, desc = oracle_sample(cfg)
+        params, st, steps, cells, desc = oracle_sample(cfg, target_s=12.0)
         with OneCore():
             t = time.perf_counter()
             oracle.run(params, *st, steps)
