@@ -1125,7 +1125,10 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
   // buffer parity); per-step diagnostics find their history slot on the
   // device, so they replay too.
   const int spl0 = !h->launches2.empty() ? 2 : 1;
-  const bool graphs = !h->multi && graphs_enabled();
+  // (the legacy and per-thread default streams cannot be captured)
+  const bool capturable = h->stream != cudaStreamLegacy && h->stream != cudaStreamPerThread &&
+                          h->stream != nullptr;
+  const bool graphs = !h->multi && capturable && graphs_enabled();
   while (graphs && nsteps >= (int64_t)kGraphPasses * spl0) {
     cudaGraphExec_t& g = h->graph[h->cur];
     if (!g || h->graph_spl != spl0) {

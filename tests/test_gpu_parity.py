@@ -612,3 +612,22 @@ def test_single_rank_nccl_machinery(halo, monkeypatch):
             ref = np.zeros(oracle.NRED)
             ref[op] = want[4][k, op]
             check_reductions(row, ref)
+
+
+def test_legacy_default_stream_long_run():
+    """A handle on the legacy default stream (binding: stream=0) takes long
+    sw2d_step calls without graph capture (that stream cannot be captured)."""
+    cfg, st = _bowl(200, 150)
+    hz, e, u, v = st
+    n = 130
+    want = oracle_run(P, st, n)
+    p = sw2d.make_params(200, 150, P["dx"], P["dy"], P["dt"], P["g"], P["eps"], P["hmin"],
+                         reduce_every_step=1 << sw2d.SW2D_RED_VOLUME, history_len=n)
+    h = sw2d.sw2d_create(p, None, 0)
+    try:
+        sw2d.sw2d_set_state(h, hz, e, u, v)
+        sw2d.sw2d_step(h, n)
+        got = sw2d.get_state(h, 200)
+    finally:
+        sw2d.sw2d_destroy(h)
+    assert_state_equal(got, want, where="legacy stream")
