@@ -168,9 +168,11 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
                    const float* u, const float* v);
 
 /* Enqueue nsteps >= 0 time steps on the handle's stream; returns before they
- * complete.  No host<->device transfer.  With nranks > 1 it exchanges the
- * 2-row halos each step (NCCL send/recv) and, if reduce_every_step != 0,
- * allreduces the per-step diagnostics. */
+ * complete.  No host<->device transfer.  Steps run two per launch where the
+ * kernels allow it, and long calls in one process replay CUDA graphs.  With
+ * nranks > 1 it exchanges the SW2D_HALO_ROWS-row halos before every pass of
+ * one or two steps (NCCL send/recv, or fused P2P stores) and, if
+ * reduce_every_step != 0, allreduces the per-step diagnostics. */
 int sw2d_step(sw2d* h, int64_t nsteps);
 
 /* Periodic output (the paper's once-per-run / per-iteration transfer

@@ -156,7 +156,7 @@ def sw2d_partition(ny: int, nranks: int, rank: int):
 
 def sw2d_halo_plan(ny: int, nranks: int, rank: int):
     """(send_south, recv_south, send_north, recv_north) first storage rows of
-    the 2-row halo messages of `rank` (-1: no neighbour)."""
+    the SW2D_HALO_ROWS-row halo messages of `rank` (-1: no neighbour)."""
     out = (ctypes.c_int64 * 4)()
     rc = load().sw2d_halo_plan(int(ny), int(nranks), int(rank), out)
     if rc < 0:
