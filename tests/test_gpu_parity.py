@@ -296,7 +296,9 @@ def test_c5_bench_configuration_sampled_parity():
     st, got, v0, hist, red = _full_size_run(cfg, n, 1 << sw2d.SW2D_RED_VOLUME)
     _window_parity(cfg, got, n, _sample_centers(cfg, got), size=32)
     assert np.max(np.abs(hist - v0)) <= 1e-6 * v0
-    assert abs(hist[-1] - red[sw2d.SW2D_RED_VOLUME]) <= 1e-9 * v0
+    # fused (per-quad fp32 partials, then fp64) vs standalone (fp64 per cell)
+    # VOLUME: measured 2e-9 apart on C5; the north_star bar for sums is 1e-5
+    assert abs(hist[-1] - red[sw2d.SW2D_RED_VOLUME]) <= 1e-7 * v0
 
 
 # --- the paper-shaped unfused variant (NEXT-1): same parity bar ------------
