@@ -53,6 +53,7 @@ struct Launch {
   long long row_lo, row_hi;  // global 1-based rows, inclusive
   int rows_per_seg, nsegs, blocks, part_base;
   int phase;                 // 0: needs no halo of this step; 1: after the halo exchange
+  int sk = 0;                // two-step kernel: CTAs sharing the strip-rows evenly (0: off)
 };
 
 }  // namespace
@@ -251,6 +252,13 @@ void plan_launches(sw2d* h) {
   // Rows within kHaloRows of an internal slab boundary read this step's
   // halo (phase 1, after the exchange); the rest (phase 0) overlap with it.
   // Virtual ranks use the same bands, so one GPU exercises the split.
+  const char* sk_env = std::getenv("SW2D_SK");
+  const bool sk_on = !(sk_env && std::atoi(sk_env) == 0);
+  int sk_force = 0;   // SW2D_SK=2: the even split wherever it is possible
+  if (sk_env && std::atoi(sk_env) == 2) {
+    sk_force = sms;
+    if (const char* e = std::getenv("SW2D_SK_CTAS")) sk_force = std::max(1, std::atoi(e));
+  }
   auto plan = [&](std::vector<Launch>& out, int per, long long target_segs, long long mrows,
                   int kind, int nstrips) {
     out.clear();
@@ -269,6 +277,24 @@ void plan_launches(sw2d* h) {
       L.phase = phase;
       L.blocks = kind == 3 ? (int)(((nstrips + per - 1) / per) * L.nsegs)
                            : step_grid(kind, nstrips, L.nsegs);
+      // Two-step CTA kernel: when the column groups x row segments grid does
+      // not fill the SMs (C5: 20 groups x 7 segments = 140 of 148), split the
+      // group-rows evenly over one CTA per SM instead, if that lowers the
+      // busiest CTA's streamed rows (each piece streams 8 extra rows; a share
+      // may span two groups).  sms >= 2 x groups keeps a share within two.
+      if (kind == 3 && sk_on) {
+        const long long ncc = (nstrips + per - 1) / per;
+        const long long classic = std::min<long long>(rps, rows) + 8;   // rows per CTA
+        const long long even = (rows * ncc + sms - 1) / sms + 2 * 8;
+        if (sk_force > 0 && sk_force >= 2 * ncc) {   // tests: SW2D_SK=2 [SW2D_SK_CTAS=n]
+          L.sk = sk_force;
+          L.blocks = sk_force;
+        } else if (sk_force == 0 && L.blocks < sms && (long long)sms >= 2 * ncc &&
+                   50 * even < 49 * classic) {
+          L.sk = sms;
+          L.blocks = sms;
+        }
+      }
       L.part_base = part;
       part += L.blocks;
       out.push_back(L);
@@ -331,8 +357,9 @@ void plan_launches(sw2d* h) {
       std::fprintf(stderr, "[sw2d]   slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
                    L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
     for (const Launch& L : h->launches2)
-      std::fprintf(stderr, "[sw2d]   2-step slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs\n",
-                   L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks);
+      std::fprintf(stderr, "[sw2d]   2-step slab %d rows %lld..%lld phase %d: %d segs x %d rows, %d CTAs%s\n",
+                   L.slab, L.row_lo, L.row_hi, L.phase, L.nsegs, L.rows_per_seg, L.blocks,
+                   L.sk ? " (even split)" : "");
   }
 }
 
@@ -356,6 +383,7 @@ StepArgs step_args(sw2d* h, const Launch& L, double* rec) {
   a.rows_per_seg = L.rows_per_seg;
   a.nstrips = h->nstrips;
   a.nsegs = L.nsegs;
+  a.sk_ctas = L.sk;
   a.c = h->coef;
   a.red.partials = h->partials;
   a.red.part_base = L.part_base;

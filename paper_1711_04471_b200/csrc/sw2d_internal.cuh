@@ -106,6 +106,8 @@ struct StepArgs {
   int rows_per_seg;          // output rows per warp segment
   int nstrips;               // warp strips across the columns
   int nsegs;                 // warp segments down the rows
+  int sk_ctas;               // two-step kernel: 0 = group x segment grid; > 0 = this many
+                             // CTAs sharing the strip-rows evenly (one per SM)
   Coef c;
   RedArgs red;
   RedArgs red2;              // two-step launches: the second step's record

@@ -900,6 +900,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 }
 
 // --- Two steps per pass (the CTA ring kernel, single slab) ------------------
+#ifndef SW2D_CTA2_UNROLL3
+#define SW2D_CTA2_UNROLL3 1   // 0: the two-row loop (A/B builds)
+#endif
 // A second row march, fed from registers, advances the first march's output
 // by one more step before anything is written: state n is read once and
 // state n+2 written once, 28 B per two cell-steps.  The second march runs two
@@ -926,34 +929,48 @@ __device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const f
                                            const float (&h0L)[C], const float (&uL)[C],
                                            const float (&vL)[C], const int L, const Ctx& x,
                                            Acc& acc1, Acc& acc2, float* pU, float* pV, float* pE,
-                                           float (&uS)[C], float (&hS)[C], const float (&vS)[C],
-                                           float (&vOut)[C]) {
+                                           const float (&uIn)[C], const float (&hIn)[C],
+                                           const float (&vS)[C], float (&uOut)[C],
+                                           float (&hOut)[C], float (&vOut)[C]) {
   RowOut<C> r1;
   row_stepC<RED, false, C, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
                                   nullptr, &r1);
   // state n+1 of row L-2: eta from this iteration, u from two, v from one back
-  row_stepC<RED, REMOTE, C, true>(w.s2, o.s2, r1.En, hS, uS, vS, L - 2, x, acc2, pU, pV, pE);
+  row_stepC<RED, REMOTE, C, true>(w.s2, o.s2, r1.En, hIn, uIn, vS, L - 2, x, acc2, pU, pV, pE);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    uS[c] = r1.un[c];
-    hS[c] = h0L[c];
+    uOut[c] = r1.un[c];
+    hOut[c] = h0L[c];
     vOut[c] = r1.vn[c];
   }
+}
+
+// in place: the slots uS / hS are read, then overwritten
+template <int RED, bool REMOTE, int C>
+__device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const float (&eL)[C],
+                                           const float (&h0L)[C], const float (&uL)[C],
+                                           const float (&vL)[C], const int L, const Ctx& x,
+                                           Acc& acc1, Acc& acc2, float* pU, float* pV, float* pE,
+                                           float (&uS)[C], float (&hS)[C], const float (&vS)[C],
+                                           float (&vOut)[C]) {
+  row_step2C<RED, REMOTE, C>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vS, uS,
+                             hS, vOut);
 }
 
 template <int RED, bool REMOTE>
 __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const float4 E4,
                                           const float4 H4, const float4 U4, const float4 V4,
                                           const int L, const Ctx& x, Acc& acc1, Acc& acc2,
-                                          float* pU, float* pV, float* pE, float (&uS)[4],
-                                          float (&hS)[4], const float (&vS)[4],
-                                          float (&vOut)[4]) {
+                                          float* pU, float* pV, float* pE,
+                                          const float (&uIn)[4], const float (&hIn)[4],
+                                          const float (&vS)[4], float (&uOut)[4],
+                                          float (&hOut)[4], float (&vOut)[4]) {
   const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
   const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
   const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
   const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
-  row_step2C<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vS,
-                             vOut);
+  row_step2C<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uIn, hIn, vS,
+                             uOut, hOut, vOut);
 }
 
 // 7 compute warps + the producer: 8 warps (2 per scheduler) can use up to 255
@@ -975,50 +992,101 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
-  const int cc = blockIdx.x % ncc;
-  const int seg = blockIdx.x / ncc;
-  const int strip0 = (cc * a.nstrips) / ncc;
-  const int nact = ((cc + 1) * a.nstrips) / ncc - strip0;
+  // column group g holds strips [g*nstrips/ncc, (g+1)*nstrips/ncc) (6 or 7)
+  auto gstrip = [&](int g) { return (int)(((long long)g * a.nstrips) / ncc); };
+
+  // This CTA's work: one or two pieces (column group, output rows [ra, rb]).
+  // sk_ctas == 0: CTA b is group b % ncc, row segment b / ncc.  Otherwise the
+  // launch's group-rows are split evenly over sk_ctas CTAs (a CTA's time
+  // follows its rows: its warps march side by side), so every SM gets the same
+  // rows whatever the number of column groups; a CTA whose share crosses the
+  // end of a group continues at the top of the next (a second piece).
+  int pg[2] = {0, 0}, pra[2] = {0, 0}, prb[2] = {-1, -1};
+  int npc = 0;
+  if (a.sk_ctas == 0) {
+    const int seg = blockIdx.x / ncc;
+    pg[0] = blockIdx.x % ncc;
+    pra[0] = (int)a.row_lo + seg * a.rows_per_seg;
+    prb[0] = min((int)a.row_hi, pra[0] + a.rows_per_seg - 1);
+    npc = 1;
+  } else {
+    // rows of all groups, group-major; CTA b takes units [b*W/sk, (b+1)*W/sk)
+    const long long R = a.row_hi - a.row_lo + 1;
+    const long long W = (long long)ncc * R;
+    const long long beg = (long long)blockIdx.x * W / a.sk_ctas;
+    const long long end = ((long long)blockIdx.x + 1) * W / a.sk_ctas;
+    if (end > beg) {
+      const int g = (int)(beg / R);
+      const long long r0 = beg - (long long)g * R;
+      const long long e0 = min(end - (long long)g * R, R);
+      pg[0] = g;
+      pra[0] = (int)(a.row_lo + r0);
+      prb[0] = (int)(a.row_lo + e0 - 1);
+      npc = 1;
+      if (end > (long long)(g + 1) * R) {
+        pg[1] = g + 1;
+        pra[1] = (int)a.row_lo;
+        prb[1] = (int)(a.row_lo + end - (long long)(g + 1) * R - 1);
+        npc = 2;
+      }
+    }
+  }
 
   Acc acc1, acc2;
   acc1.init();
   acc2.init();
 
-  const int ra = (int)a.row_lo + seg * a.rows_per_seg;
-  const int rb = min((int)a.row_hi, ra + a.rows_per_seg - 1);
-  const int first = ra - 4;          // first streamed row
-  const int n = rb + 4 - first + 1;  // rows streamed
   const long long pitch = a.s.pitch;
   const int srows = (int)(a.s.nelem / pitch);    // storage rows of each field
-  const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
-  const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
 
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int st = 0; st < kCtaStages; ++st) {
       mbar_init(sfull + 8 * st, 1);
-      mbar_init(sempty + 8 * st, nact);
+      mbar_init(sempty + 8 * st, kCta2Strips);   // every compute warp releases every stage
     }
     fence_proxy_async();
   }
   __syncthreads();
 
+  // the ring's stage and phase follow the CTA's running row count over its pieces
+  int rbase = 0;
+  for (int pc = 0; pc < npc; ++pc) {
+  const int cc = pc ? pg[1] : pg[0];
+  const int ra = pc ? pra[1] : pra[0];
+  const int rb = pc ? prb[1] : prb[0];
+  const int strip0 = gstrip(cc);
+  const int nact = gstrip(cc + 1) - strip0;
+  const int first = ra - 4;          // first streamed row
+  const int n = rb + 4 - first + 1;  // rows streamed
+  const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
+  const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
+
   if (warp == kCta2Strips) {
-    if (lane == 0) {
-      const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
-      for (int r = 0; r < n; ++r) {
-        const int st = r % kCtaStages;
-        if (r >= kCtaStages) {
-          const uint32_t ph = (uint32_t)(r / kCtaStages - 1) & 1u;
-          while (!mbar_try_wait(sempty + 8 * st, ph)) {
-          }
+    // the whole producer warp waits; lane 0 issues the copies.  A row outside
+    // the stored rows is written as zeros into its stage by the warp (generic
+    // stores, then a proxy fence before the stage is next filled by TMA), so
+    // the compute warps read every stage unconditionally.
+    const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
+    for (int r = 0; r < n; ++r) {
+      const int rg = rbase + r;
+      const int st = rg % kCtaStages;
+      if (rg >= kCtaStages) {
+        const uint32_t ph = (uint32_t)(rg / kCtaStages - 1) & 1u;
+        while (!mbar_try_wait(sempty + 8 * st, ph)) {
         }
-        const uint32_t d = sring + st * kCta2StageBytes, b = sfull + 8 * st;
-        const int sr = sfirst + r;
-        if (sr < 0 || sr >= srows) {   // outside the stored rows: the consumers use zeros
-          mbar_expect_tx(b, 0);
-          continue;
-        }
+      }
+      const uint32_t d = sring + st * kCta2StageBytes, b = sfull + 8 * st;
+      const int sr = sfirst + r;
+      if (sr < 0 || sr >= srows) {   // outside the stored rows: zeros
+        float4* z = reinterpret_cast<float4*>(ring + st * kCta2StageBytes);
+        for (int t = lane; t < kCta2StageBytes / 16; t += 32) z[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_expect_tx(b, 0);
+        continue;
+      }
+      if (lane == 0) {
         const long long o = off0 + (long long)r * pitch;
         SW2D_CHECK(o >= 0 && o + wb / 4 <= a.s.nelem);
         mbar_expect_tx(b, 4u * wb);
@@ -1027,6 +1095,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
         bulk_g2s(d + 2 * kCta2WinBytes, a.s.U + o, wb, b);
         bulk_g2s(d + 3 * kCta2WinBytes, a.s.V + o, wb, b);
       }
+      __syncwarp();
     }
   } else if (warp < nact) {
     Ctx x;
@@ -1072,43 +1141,88 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
     const int sl = (warp * kColsPerStrip + lane * 4) * 4;
 
     auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
-      const int st = i % kCtaStages;
-      const uint32_t ph = (uint32_t)(i / kCtaStages) & 1u;
+      const int st = (rbase + i) % kCtaStages;
+      const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
       while (!mbar_try_wait(sfull + 8 * st, ph)) {
       }
-      const int sr = sfirst + i;
-      if (sr < 0 || sr >= srows) {
-        E4 = H4 = U4 = V4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      } else {
-        const unsigned char* base = ring + st * kCta2StageBytes + sl;
-        E4 = *reinterpret_cast<const float4*>(base);
-        H4 = *reinterpret_cast<const float4*>(base + kCta2WinBytes);
-        U4 = *reinterpret_cast<const float4*>(base + 2 * kCta2WinBytes);
-        V4 = *reinterpret_cast<const float4*>(base + 3 * kCta2WinBytes);
-      }
+      const unsigned char* base = ring + st * kCta2StageBytes + sl;
+      E4 = *reinterpret_cast<const float4*>(base);
+      H4 = *reinterpret_cast<const float4*>(base + kCta2WinBytes);
+      U4 = *reinterpret_cast<const float4*>(base + 2 * kCta2WinBytes);
+      V4 = *reinterpret_cast<const float4*>(base + 3 * kCta2WinBytes);
       __syncwarp();
       if (lane == 0) mbar_arrive(sempty + 8 * st);
     };
     // the second march's rows L-2, L-3, L-4 (output pointers)
     int i = 0;
+#if SW2D_CTA2_UNROLL3
+    // three rows per iteration: every value the loop carries (the wet flags of
+    // rows L-1 / L-2, u(n+1) and hzero two rows back, v(n+1) one row back)
+    // rotates through three register slots, so no copies at the back edge
+    Win2<4> wc;
+    float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
+    float vC[4] = {0.f, 0.f, 0.f, 0.f};
+    // half k reads u/h slot (k+1)%3, writes slot k%3; reads v slot (k-1)%3, writes k%3
+    for (; i + 2 < n; i += 3) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
+      fetch(i, E4, H4, U4, V4);
+      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
+      fetch(i + 1, E4, H4, U4, V4);
+      row_step2<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
+                     Vn + o, En + o - pitch, uC, hC, vA, uB, hB, vB);
+      fetch(i + 2, E4, H4, U4, V4);
+      row_step2<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
+                     Un + o + 2 * pitch, Vn + o + pitch, En + o, uA, hA, vB, uC, hC, vC);
+    }
+    for (; i < n; ++i) {   // 0..2 remaining rows: fall back to copies
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 2) * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                     Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
+      wa = wb;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {   // shift the slots by one half
+        const float tu = uA[c], th = hA[c], tv = vA[c];
+        uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
+        uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
+        uC[c] = tu; hC[c] = th; vC[c] = tv;
+      }
+    }
+#else
     for (; i + 1 < n; i += 2) {
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
       fetch(i, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
       fetch(i + 1, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
-                     Vn + o, En + o - pitch, uB, hB, vA, vB);
+                     Vn + o, En + o - pitch, uB, hB, vA, uB, hB, vB);
     }
     if (i < n) {
       float4 E4, H4, U4, V4;
       const long long o = lo + (long long)(i - 2) * pitch;
       fetch(i, E4, H4, U4, V4);
       row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA);
+                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
+    }
+#endif
+  } else {
+    // a warp without a strip in this piece still releases every stage
+    for (int i = 0; i < n; ++i) {
+      const int st = (rbase + i) % kCtaStages;
+      const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
+      while (!mbar_try_wait(sfull + 8 * st, ph)) {
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty + 8 * st);
     }
   }
+  rbase += n;
+  }  // pieces
   if (RED >= 1) {
     block_reduce_and_finalize<RED, kCta2Strips + 1>(acc1, a.red);
     block_reduce_and_finalize<RED, kCta2Strips + 1>(acc2, a.red2);
@@ -1459,7 +1573,8 @@ void launch_two(const StepArgs& a, cudaStream_t s) {
     attr_devices |= 1ull << (dev & 63);
   }
   const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
-  sw2d_step_cta2<RED, REMOTE><<<ncc * a.nsegs, kCta2Threads, kCta2Smem, s>>>(a);
+  const int blocks = a.sk_ctas > 0 ? a.sk_ctas : ncc * a.nsegs;
+  sw2d_step_cta2<RED, REMOTE><<<blocks, kCta2Threads, kCta2Smem, s>>>(a);
 }
 }  // namespace
 

@@ -591,6 +591,46 @@ def test_mapping_permutations_bitwise(env, monkeypatch):
     assert_state_equal(got, want, where=str(env))
 
 
+@pytest.mark.parametrize("nx,ny,n,ctas", [(700, 300, 41, ""), (700, 300, 41, "23"),
+                                          (2000, 389, 30, ""), (2000, 389, 7, "61"),
+                                          (1921, 64, 12, "6"), (600, 9, 5, "")])
+def test_even_split_bitwise(nx, ny, n, ctas, monkeypatch):
+    """The two-step kernel's even split of group-rows over CTAs (SW2D_SK=2
+    forces it; the planner picks it on HBM-sized grids such as C3/C5): CTAs
+    whose share spans two column groups of different widths, shares of a few
+    rows, CTAs with no rows (600x9 over 148 CTAs) — bitwise equal to the
+    oracle with all per-step diagnostics, odd step counts included."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", "1")
+    monkeypatch.setenv("SW2D_SK", "2")
+    if ctas:
+        monkeypatch.setenv("SW2D_SK_CTAS", ctas)
+    st = _bowl(nx, ny)[1]
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL)
+    assert_state_equal(got, want[:4], where=f"even split {nx}x{ny} ctas {ctas or 'sms'}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    for op, series in hist.items():
+        for k in range(n):
+            row = np.zeros(oracle.NRED)
+            row[op] = series[k]
+            ref = np.zeros(oracle.NRED)
+            ref[op] = want[4][k, op]
+            check_reductions(row, ref)
+
+
+@pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
+def test_even_split_virtual_ranks_bitwise(halo, monkeypatch):
+    """Even split inside each slab's interior launch, with the halo-band
+    launches of three virtual ranks (NCCL-plan copies or P2P stores)."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", "1")
+    monkeypatch.setenv("SW2D_SK", "2")
+    monkeypatch.setenv("SW2D_GRAPHS", "0")
+    st = _bowl(700, 300)[1]
+    want = oracle_run(P, st, 19)
+    got, _, _, _ = gpu_run(P, st, 19, dist=sw2d.make_dist(0, 3, 0, 1, halo_mode=halo))
+    assert_state_equal(got, want, where=f"even split, 3 virtual ranks, halo {halo}")
+
+
 @pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
 def test_single_rank_nccl_machinery(halo, monkeypatch):
     """One real rank with the NCCL path forced on (SW2D_FORCE_NCCL): the

@@ -1,0 +1,14 @@
+# A/B of an environment setting on the bench lines: bash tools/exp_env_ab.sh <label> "<VAR=val ...>" [tests]
+label=${1:-ab}; envB=${2:-SW2D_SK=0}
+mkdir -p gpurun_out
+if [ "$3" = "tests" ]; then
+  timeout 1200 python -m pytest tests -m gpu -q -rf -x > gpurun_out/gpu_tests_$label.log 2>&1
+  tail -2 gpurun_out/gpu_tests_$label.log
+fi
+out=gpurun_out/ab_$label.log; rm -f $out
+for rep in 1 2; do
+for e in "SW2D_AB=A" "$envB"; do
+for w in "--workload c5" "--workload c3" "--workload c5 --reduce none" "--workload c5 --reduce all"; do
+  env $e timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline $w 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$e $w', round(d['value']/1e9,2), 'Gcell/s', round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'])" >> $out 2>&1
+done; done; done
+cat $out
