@@ -900,8 +900,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 }
 
 // --- Two steps per pass (the CTA ring kernel, single slab) ------------------
+#ifndef SW2D_CTA2_PIPE
+#define SW2D_CTA2_PIPE 1      // second march one row behind (A/B builds: 0)
+#endif
 #ifndef SW2D_CTA2_UNROLL3
-#define SW2D_CTA2_UNROLL3 1   // 0: the two-row loop (A/B builds)
+#define SW2D_CTA2_UNROLL3 1   // (without PIPE) 0: the two-row loop
 #endif
 // A second row march, fed from registers, advances the first march's output
 // by one more step before anything is written: state n is read once and
@@ -957,6 +960,50 @@ __device__ __forceinline__ void row_step2C(const Win2<C>& w, Win2<C>& o, const f
                              hS, vOut);
 }
 
+// Software-pipelined pair: the second march runs one loaded row further
+// behind (row L-3), on state n+1 the first march completed in earlier
+// iterations, so within one iteration the two marches are independent and
+// their dependency chains interleave (each march alone leaves the warp waiting
+// on fixed-latency results: the kernel's time follows rows, not instructions).
+//   eta(n+1) of row L-3: the first march of the previous row (slot En1, read
+//     by march 2, then overwritten with this row's),
+//   u(n+1), hzero of row L-3: three rows back (slot uS/hS, read, then
+//     overwritten), v(n+1) of row L-3: two rows back (vIn); this row's: vOut.
+template <int RED, bool REMOTE, int C>
+__device__ __forceinline__ void row_step2P(const Win2<C>& w, Win2<C>& o, const float (&eL)[C],
+                                           const float (&h0L)[C], const float (&uL)[C],
+                                           const float (&vL)[C], const int L, const Ctx& x,
+                                           Acc& acc1, Acc& acc2, float* pU, float* pV, float* pE,
+                                           float (&uS)[C], float (&hS)[C], const float (&vIn)[C],
+                                           float (&vOut)[C], float (&En1)[C]) {
+  row_stepC<RED, REMOTE, C, true>(w.s2, o.s2, En1, hS, uS, vIn, L - 3, x, acc2, pU, pV, pE);
+  RowOut<C> r1;
+  row_stepC<RED, false, C, false>(w.s1, o.s1, eL, h0L, uL, vL, L, x, acc1, nullptr, nullptr,
+                                  nullptr, &r1);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    uS[c] = r1.un[c];
+    hS[c] = h0L[c];
+    vOut[c] = r1.vn[c];
+    En1[c] = r1.En[c];
+  }
+}
+
+template <int RED, bool REMOTE>
+__device__ __forceinline__ void row_step2p(const Win2<4>& w, Win2<4>& o, const float4 E4,
+                                           const float4 H4, const float4 U4, const float4 V4,
+                                           const int L, const Ctx& x, Acc& acc1, Acc& acc2,
+                                           float* pU, float* pV, float* pE, float (&uS)[4],
+                                           float (&hS)[4], const float (&vIn)[4],
+                                           float (&vOut)[4], float (&En1)[4]) {
+  const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
+  const float h0L[4] = {H4.x, H4.y, H4.z, H4.w};
+  const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
+  const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+  row_step2P<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc1, acc2, pU, pV, pE, uS, hS, vIn,
+                             vOut, En1);
+}
+
 template <int RED, bool REMOTE>
 __device__ __forceinline__ void row_step2(const Win2<4>& w, Win2<4>& o, const float4 E4,
                                           const float4 H4, const float4 U4, const float4 V4,
@@ -984,6 +1031,9 @@ constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
 template <int RED, bool REMOTE>
 __global__ void __launch_bounds__(kCta2Threads, 1)
     sw2d_step_cta2(const StepArgs a) {
+  // with per-step diagnostics the pipelined pair is faster (C5 VOLUME +1%,
+  // all seven +0.5%); without them the plain pair (-2% pipelined)
+  constexpr bool kPipe = SW2D_CTA2_PIPE && RED >= 1;
   extern __shared__ __align__(128) unsigned char dsm[];
   unsigned char* ring = dsm;
   const uint32_t sring = smem_u32(ring);
@@ -1058,7 +1108,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
   const int strip0 = gstrip(cc);
   const int nact = gstrip(cc + 1) - strip0;
   const int first = ra - 4;          // first streamed row
-  const int n = rb + 4 - first + 1;  // rows streamed
+  const int n = rb + 4 + (kPipe ? 1 : 0) - first + 1;  // rows streamed (pipelined: one more)
   const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
   const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
 
@@ -1155,6 +1205,43 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
     };
     // the second march's rows L-2, L-3, L-4 (output pointers)
     int i = 0;
+    if constexpr (kPipe) {
+    // three rows per iteration; slots: u/h in place with period 3 (row k uses
+    // slot k % 3), v written to slot k % 3 and read from (k + 1) % 3
+    Win2<4> wc;
+    float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
+    float vC[4] = {0.f, 0.f, 0.f, 0.f};
+    float e1[4] = {0.f, 0.f, 0.f, 0.f};
+    // the second march writes u'(L-3), v'(L-4), eta'(L-5)
+    for (; i + 2 < n; i += 3) {
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
+      fetch(i, E4, H4, U4, V4);
+      row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                              Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
+      fetch(i + 1, E4, H4, U4, V4);
+      row_step2p<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2,
+                              Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vC, vB, e1);
+      fetch(i + 2, E4, H4, U4, V4);
+      row_step2p<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
+                              Un + o + 2 * pitch, Vn + o + pitch, En + o, uC, hC, vA, vC, e1);
+    }
+    for (; i < n; ++i) {   // 0..2 remaining rows: shift the slots instead
+      float4 E4, H4, U4, V4;
+      const long long o = lo + (long long)(i - 3) * pitch;
+      fetch(i, E4, H4, U4, V4);
+      row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                              Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
+      wa = wb;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float tu = uA[c], th = hA[c], tv = vA[c];
+        uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
+        uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
+        uC[c] = tu; hC[c] = th; vC[c] = tv;
+      }
+    }
+    } else {
 #if SW2D_CTA2_UNROLL3
     // three rows per iteration: every value the loop carries (the wet flags of
     // rows L-1 / L-2, u(n+1) and hzero two rows back, v(n+1) one row back)
@@ -1210,6 +1297,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
                      Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
     }
 #endif
+    }
   } else {
     // a warp without a strip in this piece still releases every stage
     for (int i = 0; i < n; ++i) {
