@@ -22,6 +22,8 @@ Q="python bench.py --profile --steps 1 --warmup 3 --substeps 4"
 timeout 600 $Q > $D/plain_prof.log 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sw2d_step -s 4 -c 1 -o $D/prof_c5 $Q > $D/ncu_prof.log 2>&1
 python tools/ncu_summary.py $D/prof_c5.ncu-rep ${label}_c5 --cells 268435456 > $D/ncu_c5.json 2>&1; echo "prof rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sw2d_step -s 4 -c 1 -o $D/prof_c3 $Q --workload c3 > $D/ncu_prof_c3.log 2>&1
+python tools/ncu_summary.py $D/prof_c3.ncu-rep ${label}_c3 --cells 67108864 > $D/ncu_c3.json 2>&1; echo "prof c3 rc=$?"
 python - <<P
 import json
 for f in ["$D/bench.jsonl","$D/bench_reference.jsonl","$D/bench_more.jsonl"]:
