@@ -341,10 +341,12 @@ void plan_launches(sw2d* h) {
     char buf[256];
     std::snprintf(buf, sizeof(buf),
                   "kernel=%s steps_per_launch=%d launches_per_pass=%zu strips=%d "
-                  "ctas_per_sm=%d halo=%s temporal_blocking=%d",
+                  "ctas_per_sm=%d halo=%s temporal_blocking=%d split=%s",
                   kinds[h->kind], h->launches2.empty() ? 1 : 2,
                   h->launches2.empty() ? h->launches.size() : h->launches2.size(), h->nstrips,
-                  bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k);
+                  bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k,
+                  std::any_of(h->launches2.begin(), h->launches2.end(),
+                              [](const Launch& L) { return L.sk > 0; }) ? "even-rows" : "grid");
     h->plan_text = buf;
   }
   if (std::getenv("SW2D_VERBOSE")) {

@@ -749,7 +749,10 @@ constexpr int kCtaStrips = 8;
 #define SW2D_CTA_EXIT_BARRIER 1
 #endif
 constexpr bool kCtaBarrierAtExit = SW2D_CTA_EXIT_BARRIER;
-constexpr int kCtaStages = 6;
+#ifndef SW2D_CTA_STAGES
+#define SW2D_CTA_STAGES 6
+#endif
+constexpr int kCtaStages = SW2D_CTA_STAGES;   // ring rows of the CTA kernels
 constexpr int kCtaWinBytes = (kCtaStrips * kColsPerStrip + 8) * 4;   // one field, one row
 constexpr int kCtaStageBytes = 4 * kCtaWinBytes;
 constexpr int kCtaThreads = 32 * (kCtaStrips + 1);

@@ -618,6 +618,20 @@ def test_even_split_bitwise(nx, ny, n, ctas, monkeypatch):
             check_reductions(row, ref)
 
 
+@pytest.mark.parametrize("nx,ny,want", [(16384, 16384, "even-rows"), (8192, 8192, "even-rows"),
+                                         (2000, 2000, "grid")])
+def test_even_split_planner_choice(nx, ny, want):
+    """The planner takes the even row split where it shortens the busiest
+    CTA's rows (C5, C3: 20 / 10 column groups leave SMs idle in the group x
+    segment grid) and keeps the grid where the split's extra streamed rows
+    would cost more (2000^2: 3 groups, ~40 rows per CTA)."""
+    h = sw2d.sw2d_create(sw2d.make_params(nx, ny), None)
+    try:
+        assert ("split=%s" % want) in sw2d.sw2d_plan(h), sw2d.sw2d_plan(h)
+    finally:
+        sw2d.sw2d_destroy(h)
+
+
 @pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
 def test_even_split_virtual_ranks_bitwise(halo, monkeypatch):
     """Even split inside each slab's interior launch, with the halo-band
