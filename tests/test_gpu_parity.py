@@ -594,22 +594,24 @@ def test_mapping_permutations_bitwise(env, monkeypatch):
 @pytest.mark.parametrize("nx,ny,n,ctas", [(700, 300, 41, ""), (700, 300, 41, "23"),
                                           (2000, 389, 30, ""), (2000, 389, 7, "61"),
                                           (1921, 64, 12, "6"), (600, 9, 5, "")])
-def test_even_split_bitwise(nx, ny, n, ctas, monkeypatch):
+@pytest.mark.parametrize("mask", [ALL, 1 << sw2d.SW2D_RED_VOLUME, 0])
+def test_even_split_bitwise(nx, ny, n, ctas, mask, monkeypatch):
     """The two-step kernel's even split of group-rows over CTAs (SW2D_SK=2
     forces it; the planner picks it on HBM-sized grids such as C3/C5): CTAs
     whose share spans two column groups of different widths, shares of a few
     rows, CTAs with no rows (600x9 over 148 CTAs) — bitwise equal to the
-    oracle with all per-step diagnostics, odd step counts included."""
+    oracle with all, one (VOLUME: the pipelined pair) or no per-step
+    diagnostics, odd step counts included."""
     monkeypatch.setenv("SW2D_STEP_KERNEL", "1")
     monkeypatch.setenv("SW2D_SK", "2")
     if ctas:
         monkeypatch.setenv("SW2D_SK_CTAS", ctas)
     st = _bowl(nx, ny)[1]
     want = oracle_run(P, st, n, history=True)
-    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=mask)
     assert_state_equal(got, want[:4], where=f"even split {nx}x{ny} ctas {ctas or 'sms'}")
     check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
-    for op, series in hist.items():
+    for op, series in (hist or {}).items():
         for k in range(n):
             row = np.zeros(oracle.NRED)
             row[op] = series[k]
