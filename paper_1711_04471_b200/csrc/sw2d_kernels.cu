@@ -1105,214 +1105,215 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
   // the ring's stage and phase follow the CTA's running row count over its pieces
   int rbase = 0;
   for (int pc = 0; pc < npc; ++pc) {
-  const int cc = pc ? pg[1] : pg[0];
-  const int ra = pc ? pra[1] : pra[0];
-  const int rb = pc ? prb[1] : prb[0];
-  const int strip0 = gstrip(cc);
-  const int nact = gstrip(cc + 1) - strip0;
-  const int first = ra - 4;          // first streamed row
-  const int n = rb + 4 + (kPipe ? 1 : 0) - first + 1;  // rows streamed (pipelined: one more)
-  const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
-  const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
+    const int cc = pc ? pg[1] : pg[0];
+    const int ra = pc ? pra[1] : pra[0];
+    const int rb = pc ? prb[1] : prb[0];
+    const int strip0 = gstrip(cc);
+    const int nact = gstrip(cc + 1) - strip0;
+    const int first = ra - 4;          // first streamed row
+    const int n = rb + 4 + (kPipe ? 1 : 0) - first + 1;  // rows streamed (pipelined: one more)
+    const int sfirst = first - (int)a.s.jbase;      // storage row of `first` (may be < 0)
+    const long long off0 = (long long)sfirst * pitch + strip0 * kColsPerStrip + kStripBase;
 
-  if (warp == kCta2Strips) {
-    // the whole producer warp waits; lane 0 issues the copies.  A row outside
-    // the stored rows is written as zeros into its stage by the warp (generic
-    // stores, then a proxy fence before the stage is next filled by TMA), so
-    // the compute warps read every stage unconditionally.
-    const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
-    for (int r = 0; r < n; ++r) {
-      const int rg = rbase + r;
-      const int st = rg % kCtaStages;
-      if (rg >= kCtaStages) {
-        const uint32_t ph = (uint32_t)(rg / kCtaStages - 1) & 1u;
-        while (!mbar_try_wait(sempty + 8 * st, ph)) {
+    if (warp == kCta2Strips) {
+      // the whole producer warp waits; lane 0 issues the copies.  A row outside
+      // the stored rows is written as zeros into its stage by the warp (generic
+      // stores, then a proxy fence before the stage is next filled by TMA), so
+      // the compute warps read every stage unconditionally.
+      const uint32_t wb = (uint32_t)(nact * kColsPerStrip + 8) * 4u;
+      for (int r = 0; r < n; ++r) {
+        const int rg = rbase + r;
+        const int st = rg % kCtaStages;
+        if (rg >= kCtaStages) {
+          const uint32_t ph = (uint32_t)(rg / kCtaStages - 1) & 1u;
+          while (!mbar_try_wait(sempty + 8 * st, ph)) {
+          }
         }
-      }
-      const uint32_t d = sring + st * kCta2StageBytes, b = sfull + 8 * st;
-      const int sr = sfirst + r;
-      if (sr < 0 || sr >= srows) {   // outside the stored rows: zeros
-        float4* z = reinterpret_cast<float4*>(ring + st * kCta2StageBytes);
-        for (int t = lane; t < kCta2StageBytes / 16; t += 32) z[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        fence_proxy_async();
+        const uint32_t d = sring + st * kCta2StageBytes, b = sfull + 8 * st;
+        const int sr = sfirst + r;
+        if (sr < 0 || sr >= srows) {   // outside the stored rows: zeros
+          float4* z = reinterpret_cast<float4*>(ring + st * kCta2StageBytes);
+          for (int t = lane; t < kCta2StageBytes / 16; t += 32)
+            z[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) mbar_expect_tx(b, 0);
+          continue;
+        }
+        if (lane == 0) {
+          const long long o = off0 + (long long)r * pitch;
+          SW2D_CHECK(o >= 0 && o + wb / 4 <= a.s.nelem);
+          mbar_expect_tx(b, 4u * wb);
+          bulk_g2s(d, a.s.E + o, wb, b);
+          bulk_g2s(d + kCta2WinBytes, a.s.H0 + o, wb, b);
+          bulk_g2s(d + 2 * kCta2WinBytes, a.s.U + o, wb, b);
+          bulk_g2s(d + 3 * kCta2WinBytes, a.s.V + o, wb, b);
+        }
         __syncwarp();
-        if (lane == 0) mbar_expect_tx(b, 0);
-        continue;
       }
-      if (lane == 0) {
-        const long long o = off0 + (long long)r * pitch;
-        SW2D_CHECK(o >= 0 && o + wb / 4 <= a.s.nelem);
-        mbar_expect_tx(b, 4u * wb);
-        bulk_g2s(d, a.s.E + o, wb, b);
-        bulk_g2s(d + kCta2WinBytes, a.s.H0 + o, wb, b);
-        bulk_g2s(d + 2 * kCta2WinBytes, a.s.U + o, wb, b);
-        bulk_g2s(d + 3 * kCta2WinBytes, a.s.V + o, wb, b);
-      }
-      __syncwarp();
-    }
-  } else if (warp < nact) {
-    Ctx x;
-    x.ra = ra;
-    x.rb = rb;
-    const int c0 = (strip0 + warp) * kColsPerStrip + kStripBase + lane * 4;
-    const int k0 = c0 - kColOff;
-    x.colmask = 0;
-    x.umask = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
-      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
-      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
-    }
-    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
-    x.q = a.c.q; x.hmin = a.c.hmin;
-    x.ny = (int)a.ny;
-    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
-    x.col = c0;
-    x.pitch = pitch;
-    x.rem = a.rem;
-#ifdef SW2D_DEBUG_BOUNDS
-    x.dU = a.s.Un;
-    x.dV = a.s.Vn;
-    x.dE = a.s.En;
-    x.nelem = a.s.nelem;
-#endif
-    Win2<4> wa, wb;
-    wa.zero();
-    float uA[4] = {0.f, 0.f, 0.f, 0.f}, uB[4] = {0.f, 0.f, 0.f, 0.f};
-    float hA[4] = {0.f, 0.f, 0.f, 0.f}, hB[4] = {0.f, 0.f, 0.f, 0.f};
-    // v(n+1) of the row one iteration back, alternating slots (no copies)
-    float vA[4] = {0.f, 0.f, 0.f, 0.f}, vB[4] = {0.f, 0.f, 0.f, 0.f};
-    float* __restrict__ En = a.s.En;
-    float* __restrict__ Un = a.s.Un;
-    float* __restrict__ Vn = a.s.Vn;
-    const long long lo = off0 + warp * kColsPerStrip + lane * 4;
-    const int sl = (warp * kColsPerStrip + lane * 4) * 4;
-
-    auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
-      const int st = (rbase + i) % kCtaStages;
-      const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
-      while (!mbar_try_wait(sfull + 8 * st, ph)) {
-      }
-      const unsigned char* base = ring + st * kCta2StageBytes + sl;
-      E4 = *reinterpret_cast<const float4*>(base);
-      H4 = *reinterpret_cast<const float4*>(base + kCta2WinBytes);
-      U4 = *reinterpret_cast<const float4*>(base + 2 * kCta2WinBytes);
-      V4 = *reinterpret_cast<const float4*>(base + 3 * kCta2WinBytes);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sempty + 8 * st);
-    };
-    // the second march's rows L-2, L-3, L-4 (output pointers)
-    int i = 0;
-    if constexpr (kPipe) {
-    // three rows per iteration; slots: u/h in place with period 3 (row k uses
-    // slot k % 3), v written to slot k % 3 and read from (k + 1) % 3
-    Win2<4> wc;
-    float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
-    float vC[4] = {0.f, 0.f, 0.f, 0.f};
-    float e1[4] = {0.f, 0.f, 0.f, 0.f};
-    // the second march writes u'(L-3), v'(L-4), eta'(L-5)
-    for (; i + 2 < n; i += 3) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
-      fetch(i, E4, H4, U4, V4);
-      row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                              Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
-      fetch(i + 1, E4, H4, U4, V4);
-      row_step2p<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2,
-                              Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vC, vB, e1);
-      fetch(i + 2, E4, H4, U4, V4);
-      row_step2p<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
-                              Un + o + 2 * pitch, Vn + o + pitch, En + o, uC, hC, vA, vC, e1);
-    }
-    for (; i < n; ++i) {   // 0..2 remaining rows: shift the slots instead
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 3) * pitch;
-      fetch(i, E4, H4, U4, V4);
-      row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                              Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
-      wa = wb;
+    } else if (warp < nact) {
+      Ctx x;
+      x.ra = ra;
+      x.rb = rb;
+      const int c0 = (strip0 + warp) * kColsPerStrip + kStripBase + lane * 4;
+      const int k0 = c0 - kColOff;
+      x.colmask = 0;
+      x.umask = 0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const float tu = uA[c], th = hA[c], tv = vA[c];
-        uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
-        uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
-        uC[c] = tu; hC[c] = th; vC[c] = tv;
+        x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
+        x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
       }
-    }
-    } else {
-#if SW2D_CTA2_UNROLL3
-    // three rows per iteration: every value the loop carries (the wet flags of
-    // rows L-1 / L-2, u(n+1) and hzero two rows back, v(n+1) one row back)
-    // rotates through three register slots, so no copies at the back edge
-    Win2<4> wc;
-    float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
-    float vC[4] = {0.f, 0.f, 0.f, 0.f};
-    // half k reads u/h slot (k+1)%3, writes slot k%3; reads v slot (k-1)%3, writes k%3
-    for (; i + 2 < n; i += 3) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
-      fetch(i, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
-      fetch(i + 1, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
-                     Vn + o, En + o - pitch, uC, hC, vA, uB, hB, vB);
-      fetch(i + 2, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
-                     Un + o + 2 * pitch, Vn + o + pitch, En + o, uA, hA, vB, uC, hC, vC);
-    }
-    for (; i < n; ++i) {   // 0..2 remaining rows: fall back to copies
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 2) * pitch;
-      fetch(i, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
-      wa = wb;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {   // shift the slots by one half
-        const float tu = uA[c], th = hA[c], tv = vA[c];
-        uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
-        uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
-        uC[c] = tu; hC[c] = th; vC[c] = tv;
+      for (int c = 0; c < 4; ++c) {
+        x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
+        x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
       }
-    }
-#else
-    for (; i + 1 < n; i += 2) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
-      fetch(i, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
-      fetch(i + 1, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
-                     Vn + o, En + o - pitch, uB, hB, vA, uB, hB, vB);
-    }
-    if (i < n) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)(i - 2) * pitch;
-      fetch(i, E4, H4, U4, V4);
-      row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
-                     Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
-    }
+      x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+      x.q = a.c.q; x.hmin = a.c.hmin;
+      x.ny = (int)a.ny;
+      x.out_lane = (lane >= 1) && (lane <= kOutLanes);
+      x.col = c0;
+      x.pitch = pitch;
+      x.rem = a.rem;
+#ifdef SW2D_DEBUG_BOUNDS
+      x.dU = a.s.Un;
+      x.dV = a.s.Vn;
+      x.dE = a.s.En;
+      x.nelem = a.s.nelem;
 #endif
-    }
-  } else {
-    // a warp without a strip in this piece still releases every stage
-    for (int i = 0; i < n; ++i) {
-      const int st = (rbase + i) % kCtaStages;
-      const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
-      while (!mbar_try_wait(sfull + 8 * st, ph)) {
+      Win2<4> wa, wb;
+      wa.zero();
+      float uA[4] = {0.f, 0.f, 0.f, 0.f}, uB[4] = {0.f, 0.f, 0.f, 0.f};
+      float hA[4] = {0.f, 0.f, 0.f, 0.f}, hB[4] = {0.f, 0.f, 0.f, 0.f};
+      // v(n+1) of the row one iteration back, alternating slots (no copies)
+      float vA[4] = {0.f, 0.f, 0.f, 0.f}, vB[4] = {0.f, 0.f, 0.f, 0.f};
+      float* __restrict__ En = a.s.En;
+      float* __restrict__ Un = a.s.Un;
+      float* __restrict__ Vn = a.s.Vn;
+      const long long lo = off0 + warp * kColsPerStrip + lane * 4;
+      const int sl = (warp * kColsPerStrip + lane * 4) * 4;
+
+      auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
+        const int st = (rbase + i) % kCtaStages;
+        const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
+        while (!mbar_try_wait(sfull + 8 * st, ph)) {
+        }
+        const unsigned char* base = ring + st * kCta2StageBytes + sl;
+        E4 = *reinterpret_cast<const float4*>(base);
+        H4 = *reinterpret_cast<const float4*>(base + kCta2WinBytes);
+        U4 = *reinterpret_cast<const float4*>(base + 2 * kCta2WinBytes);
+        V4 = *reinterpret_cast<const float4*>(base + 3 * kCta2WinBytes);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty + 8 * st);
+      };
+      // the second march's rows L-2, L-3, L-4 (output pointers)
+      int i = 0;
+      if constexpr (kPipe) {
+      // three rows per iteration; slots: u/h in place with period 3 (row k uses
+      // slot k % 3), v written to slot k % 3 and read from (k + 1) % 3
+      Win2<4> wc;
+      float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
+      float vC[4] = {0.f, 0.f, 0.f, 0.f};
+      float e1[4] = {0.f, 0.f, 0.f, 0.f};
+      // the second march writes u'(L-3), v'(L-4), eta'(L-5)
+      for (; i + 2 < n; i += 3) {
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
+        fetch(i, E4, H4, U4, V4);
+        row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
+        fetch(i + 1, E4, H4, U4, V4);
+        row_step2p<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2,
+                                Un + o + pitch, Vn + o, En + o - pitch, uB, hB, vC, vB, e1);
+        fetch(i + 2, E4, H4, U4, V4);
+        row_step2p<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
+                                Un + o + 2 * pitch, Vn + o + pitch, En + o, uC, hC, vA, vC, e1);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sempty + 8 * st);
+      for (; i < n; ++i) {   // 0..2 remaining rows: shift the slots instead
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 3) * pitch;
+        fetch(i, E4, H4, U4, V4);
+        row_step2p<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                                Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, vA, e1);
+        wa = wb;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float tu = uA[c], th = hA[c], tv = vA[c];
+          uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
+          uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
+          uC[c] = tu; hC[c] = th; vC[c] = tv;
+        }
+      }
+      } else {
+#if SW2D_CTA2_UNROLL3
+      // three rows per iteration: every value the loop carries (the wet flags of
+      // rows L-1 / L-2, u(n+1) and hzero two rows back, v(n+1) one row back)
+      // rotates through three register slots, so no copies at the back edge
+      Win2<4> wc;
+      float uC[4] = {0.f, 0.f, 0.f, 0.f}, hC[4] = {0.f, 0.f, 0.f, 0.f};
+      float vC[4] = {0.f, 0.f, 0.f, 0.f};
+      // half k reads u/h slot (k+1)%3, writes slot k%3; reads v slot (k-1)%3, writes k%3
+      for (; i + 2 < n; i += 3) {
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
+        fetch(i, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                       Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
+        fetch(i + 1, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wb, wc, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
+                       Vn + o, En + o - pitch, uC, hC, vA, uB, hB, vB);
+        fetch(i + 2, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
+                       Un + o + 2 * pitch, Vn + o + pitch, En + o, uA, hA, vB, uC, hC, vC);
+      }
+      for (; i < n; ++i) {   // 0..2 remaining rows: fall back to copies
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 2) * pitch;
+        fetch(i, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                       Vn + o - pitch, En + o - 2 * pitch, uB, hB, vC, uA, hA, vA);
+        wa = wb;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {   // shift the slots by one half
+          const float tu = uA[c], th = hA[c], tv = vA[c];
+          uA[c] = uB[c]; hA[c] = hB[c]; vA[c] = vB[c];
+          uB[c] = uC[c]; hB[c] = hC[c]; vB[c] = vC[c];
+          uC[c] = tu; hC[c] = th; vC[c] = tv;
+        }
+      }
+#else
+      for (; i + 1 < n; i += 2) {
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 2) * pitch;   // row first + i - 2
+        fetch(i, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                       Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
+        fetch(i + 1, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc1, acc2, Un + o + pitch,
+                       Vn + o, En + o - pitch, uB, hB, vA, uB, hB, vB);
+      }
+      if (i < n) {
+        float4 E4, H4, U4, V4;
+        const long long o = lo + (long long)(i - 2) * pitch;
+        fetch(i, E4, H4, U4, V4);
+        row_step2<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc1, acc2, Un + o,
+                       Vn + o - pitch, En + o - 2 * pitch, uA, hA, vB, uA, hA, vA);
+      }
+#endif
+      }
+    } else {
+      // a warp without a strip in this piece still releases every stage
+      for (int i = 0; i < n; ++i) {
+        const int st = (rbase + i) % kCtaStages;
+        const uint32_t ph = (uint32_t)((rbase + i) / kCtaStages) & 1u;
+        while (!mbar_try_wait(sfull + 8 * st, ph)) {
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty + 8 * st);
+      }
     }
-  }
-  rbase += n;
+    rbase += n;
   }  // pieces
   if (RED >= 1) {
     block_reduce_and_finalize<RED, kCta2Strips + 1>(acc1, a.red);
