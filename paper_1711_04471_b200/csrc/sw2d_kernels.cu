@@ -299,6 +299,7 @@ struct Ctx {
   unsigned umask;    // columns 1..nx-1 (faces that are not the east wall)
   float cmf[4];      // colmask as 1.0 / 0.0 per column
   float umf[4];      // umask as 1.0 / 0.0 per column
+  float cgxc[4];     // cgx on faces that are not walls (umask), 0 on wall / outside faces
   int ny, ra, rb;    // global rows (1-based): grid rows, this segment's output rows
   bool out_lane;
   int col;                 // storage column of this lane's element 0 (REMOTE only)
@@ -396,15 +397,22 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   const float wR = __shfl_down_sync(kFull, wL[0], 1);
   const float wLf = __shfl_up_sync(kFull, wL[C - 1], 1);
 
-  // a2: un(L) on the east faces of row L; vn(L-1) on the north faces of L-1
-  const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north wall
+  // a2: un(L) on the east faces of row L; vn(L-1) on the north faces of L-1.
+  // East/west wall faces (and faces outside the grid) must come out 0: their
+  // pressure-gradient coefficient is taken as 0 (cgxc, per column), so the
+  // face rule reduces to wc && wn, and such a face always has a dry cell (the
+  // halo) on one side: blocked -> 0, with no per-cell mask multiply.  Every
+  // other face keeps cgx and the arithmetic of §4.  (The same trick per row
+  // for the north/south walls made ptxas emit more selects: the row select
+  // stays.)
+  const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north / south wall
   float un[C], vn[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float en = (c < C - 1) ? eL[c + 1] : eR;
     const float wn = (c < C - 1) ? wL[c + 1] : wR;
-    const float du = __fmul_rn(x.cgx, __fsub_rn(en, eL[c]));
-    un[c] = __fmul_rn(face(wL[c] != 0.0f, wn != 0.0f, du, uL[c]), x.umf[c]);
+    const float du = __fmul_rn(x.cgxc[c], __fsub_rn(en, eL[c]));
+    un[c] = face(wL[c] != 0.0f, wn != 0.0f, du, uL[c]);
     const float dv = __fmul_rn(x.cgy, __fsub_rn(eL[c], w.e[c]));
     const float v = face(w.w1[c] != 0.0f, wL[c] != 0.0f, dv, w.v[c]);
     vn[c] = vrow ? v : 0.0f;
@@ -631,6 +639,7 @@ __global__ void __launch_bounds__(32 * kStepWarps)
       x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
@@ -840,6 +849,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
       x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
@@ -1170,6 +1180,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
         x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
       }
       x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+      for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
       x.q = a.c.q; x.hmin = a.c.hmin;
       x.ny = (int)a.ny;
       x.out_lane = (lane >= 1) && (lane <= kOutLanes);
@@ -1370,6 +1381,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
       x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
@@ -1455,6 +1467,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps, SW2D_SMALL2_MINB)
       x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
+    for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
     x.q = a.c.q; x.hmin = a.c.hmin;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 2) && (lane <= 29);

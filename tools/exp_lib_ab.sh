@@ -8,7 +8,7 @@ fi
 out=gpurun_out/ab_$label.log; rm -f $out
 for rep in 1 2; do
 for lib in paper_1711_04471_b200/libsw2d.so $libB; do
-for w in "--workload c5" "--workload c3" "--workload c5 --reduce none" "--workload c5 --reduce all"; do
+for w in "--workload c5" "--workload c3" "--workload c5 --reduce all" "--workload p1000 --substeps 1000"; do
   SW2D_LIBRARY=$lib timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline $w 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$(basename $lib) $w', round(d['value']/1e9,2), 'Gcell/s', round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'])" >> $out 2>&1
 done; done; done
 cat $out
