@@ -242,6 +242,8 @@ void plan_tb(sw2d* h, int sms) {
   h->tb_k = K;
 }
 
+constexpr int kSkReserveSms = 4;   // SMs left free by the even split with real ranks
+
 void plan_launches(sw2d* h) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
@@ -282,17 +284,21 @@ void plan_launches(sw2d* h) {
       // group-rows evenly over one CTA per SM instead, if that lowers the
       // busiest CTA's streamed rows (each piece streams 8 extra rows; a share
       // may span two groups).  sms >= 2 x groups keeps a share within two.
+      // With real ranks a few SMs stay free: a step CTA holds a whole SM
+      // (registers), so the halo exchange's NCCL kernels and the boundary-band
+      // launches that overlap the interior launch need SMs of their own.
       if (kind == 3 && sk_on) {
         const long long ncc = (nstrips + per - 1) / per;
+        const long long skc = h->multi ? std::max(1, sms - kSkReserveSms) : sms;
         const long long classic = std::min<long long>(rps, rows) + 8;   // rows per CTA
-        const long long even = (rows * ncc + sms - 1) / sms + 2 * 8;
+        const long long even = (rows * ncc + skc - 1) / skc + 2 * 8;
         if (sk_force > 0 && sk_force >= 2 * ncc) {   // tests: SW2D_SK=2 [SW2D_SK_CTAS=n]
           L.sk = sk_force;
           L.blocks = sk_force;
-        } else if (sk_force == 0 && L.blocks < sms && (long long)sms >= 2 * ncc &&
+        } else if (sk_force == 0 && L.blocks < skc && skc >= 2 * ncc &&
                    50 * even < 49 * classic) {
-          L.sk = sms;
-          L.blocks = sms;
+          L.sk = (int)skc;
+          L.blocks = (int)skc;
         }
       }
       L.part_base = part;
@@ -338,6 +344,9 @@ void plan_launches(sw2d* h) {
   plan_tb(h, sms);
   {
     static const char* kinds[] = {"warp-ring", "cta-ring", "small"};
+    std::string split = "grid";   // even-rows:<CTAs> if any two-step launch splits rows
+    for (const Launch& L : h->launches2)
+      if (L.sk > 0) split = "even-rows:" + std::to_string(L.sk);
     char buf[256];
     std::snprintf(buf, sizeof(buf),
                   "kernel=%s steps_per_launch=%d launches_per_pass=%zu strips=%d "
@@ -345,8 +354,7 @@ void plan_launches(sw2d* h) {
                   kinds[h->kind], h->launches2.empty() ? 1 : 2,
                   h->launches2.empty() ? h->launches.size() : h->launches2.size(), h->nstrips,
                   bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k,
-                  std::any_of(h->launches2.begin(), h->launches2.end(),
-                              [](const Launch& L) { return L.sk > 0; }) ? "even-rows" : "grid");
+                  split.c_str());
     h->plan_text = buf;
   }
   if (std::getenv("SW2D_VERBOSE")) {
