@@ -335,19 +335,73 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
   return (unsigned)(r - lo) <= (unsigned)(hi - lo);
 }
 
-// Upwind flux s > 0 ? s*hL : (s < 0 ? s*hR : 0) as s * (s > 0 ? hL : hR):
-// equal in value for finite depths (s = 0 gives a zero either way).
-__device__ __forceinline__ float flux(float s, float hl, float hr) {
-  return __fmul_rn(s, s > 0.0f ? hl : hr);
-}
-
+// Upwind flux s > 0 ? s*hL : (s < 0 ? s*hR : 0) is computed as
+// s * (s > 0 ? hL : hR): equal in value for finite depths (s = 0 gives a zero
+// either way).
 // Wet/dry face rule (reading R4): the face between a cell with wet flag wc
 // and its east/north neighbour (wn) carries flow iff
 // wc ? (wn || d > 0) : (wn && d < 0); a blocked face gets 0.
-__device__ __forceinline__ float face(bool wc, bool wn, float d, float old) {
-  const bool flow = (wc & (wn | (d > 0.0f))) | (wn & (d < 0.0f));
-  return flow ? __fadd_rn(old, d) : 0.0f;
+__device__ __forceinline__ bool face_flow(bool wc, bool wn, float d) {
+  return (wc & (wn | (d > 0.0f))) | (wn & (d < 0.0f));
 }
+
+// Column-parallel FP32 arithmetic on C-column arrays.  sm_100a issues the
+// packed add/sub/mul.rn.f32x2 (SASS FADD2 / FMUL2) at the scalar instruction
+// rate (tools/f32x2_probe.cu: 3.7 warp-instructions/clk/SM either way), so a
+// pair of columns costs one issue slot.  Each element is rounded to nearest
+// exactly like __fadd_rn / __fsub_rn / __fmul_rn (no FTZ): bitwise the same
+// results.  SW2D_F32X2=0 builds the scalar form (A/B).
+//
+// ptxas (CUDA 12.9) contracts a packed mul.rn.f32x2 feeding a packed add or
+// subtract into FFMA2 even under --fmad=false (one rounding instead of two;
+// also when the add is written as an FMA with a unit multiplier).  A scalar
+// FMUL feeding a packed add, or a packed FMUL feeding a scalar add, is left
+// alone, so only the adds and subtracts are packed (17 of the 31 FP32
+// operations per cell and step); the products stay scalar (vmul).
+#ifndef SW2D_F32X2
+#define SW2D_F32X2 1
+#endif
+#define SW2D_PAIR_ASM(PTXOP)                                                                 \
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t" PTXOP      \
+      " rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"                                                 \
+      : "=f"(d0), "=f"(d1)                                                                   \
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1))
+__device__ __forceinline__ void vadd2(float& d0, float& d1, float a0, float a1, float b0,
+                                      float b1) {
+  SW2D_PAIR_ASM("add.rn.f32x2");
+}
+__device__ __forceinline__ void vsub2(float& d0, float& d1, float a0, float a1, float b0,
+                                      float b1) {
+  SW2D_PAIR_ASM("sub.rn.f32x2");
+}
+__device__ __forceinline__ void vmul2(float& d0, float& d1, float a0, float a1, float b0,
+                                      float b1) {
+  d0 = __fmul_rn(a0, b0);
+  d1 = __fmul_rn(a1, b1);
+}
+#undef SW2D_PAIR_ASM
+#define SW2D_PAIR_OP(NAME, SCALAR)                                                          \
+  template <int C>                                                                           \
+  __device__ __forceinline__ void NAME(float (&d)[C], const float (&a)[C],                   \
+                                       const float (&b)[C]) {                                \
+    _Pragma("unroll") for (int c = 0; c < C; c += (SW2D_F32X2 ? 2 : 1)) {                    \
+      if (SW2D_F32X2 && c + 1 < C) {                                                         \
+        NAME##2(d[c], d[c + 1], a[c], a[c + 1], b[c], b[c + 1]);                             \
+      } else {                                                                               \
+        d[c] = SCALAR(a[c], b[c]);                                                           \
+      }                                                                                      \
+    }                                                                                        \
+  }                                                                                          \
+  template <int C>                                                                           \
+  __device__ __forceinline__ void NAME(float (&d)[C], const float a, const float (&b)[C]) {  \
+    float aa[C];                                                                             \
+    _Pragma("unroll") for (int c = 0; c < C; ++c) aa[c] = a;                                 \
+    NAME<C>(d, aa, b);                                                                       \
+  }
+SW2D_PAIR_OP(vadd, __fadd_rn)
+SW2D_PAIR_OP(vsub, __fsub_rn)
+SW2D_PAIR_OP(vmul, __fmul_rn)
+#undef SW2D_PAIR_OP
 
 // One loaded row L: reads the window `w` (rows L-1, L-2), writes `o`.
 // C consecutive floats of a row (C = 4: float4, C = 2: float2)
@@ -387,11 +441,9 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   // 1..nx are dry)
   const bool rowok = in_rows(L, 1, x.ny);
   float hL[C], wL[C];
+  vadd<C>(hL, h0L, eL);
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    hL[c] = __fadd_rn(h0L[c], eL[c]);
-    wL[c] = (rowok && !(hL[c] < x.hmin)) ? x.cmf[c] : 0.0f;
-  }
+  for (int c = 0; c < C; ++c) wL[c] = (rowok && !(hL[c] < x.hmin)) ? x.cmf[c] : 0.0f;
   const float eR = __shfl_down_sync(kFull, eL[0], 1);
   const float hR = __shfl_down_sync(kFull, hL[0], 1);
   const float wR = __shfl_down_sync(kFull, wL[0], 1);
@@ -406,55 +458,80 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   // for the north/south walls made ptxas emit more selects: the row select
   // stays.)
   const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north / south wall
-  float un[C], vn[C];
+  // (the arithmetic below is column-parallel: vadd / vsub / vmul, same
+  // operations and operand order as the scalar form)
+  float en[C], du[C], dv[C], su[C], sv[C], un[C], vn[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) en[c] = (c < C - 1) ? eL[c + 1] : eR;
+  vsub<C>(du, en, eL);
+  float cg[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) cg[c] = x.cgxc[c];
+  vmul<C>(du, cg, du);
+  vsub<C>(dv, eL, w.e);
+  vmul<C>(dv, x.cgy, dv);
+  vadd<C>(su, uL, du);
+  vadd<C>(sv, w.v, dv);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const float en = (c < C - 1) ? eL[c + 1] : eR;
     const float wn = (c < C - 1) ? wL[c + 1] : wR;
-    const float du = __fmul_rn(x.cgxc[c], __fsub_rn(en, eL[c]));
-    un[c] = face(wL[c] != 0.0f, wn != 0.0f, du, uL[c]);
-    const float dv = __fmul_rn(x.cgy, __fsub_rn(eL[c], w.e[c]));
-    const float v = face(w.w1[c] != 0.0f, wL[c] != 0.0f, dv, w.v[c]);
-    vn[c] = vrow ? v : 0.0f;
+    un[c] = face_flow(wL[c] != 0.0f, wn != 0.0f, du[c]) ? su[c] : 0.0f;
+    const bool fv = face_flow(w.w1[c] != 0.0f, wL[c] != 0.0f, dv[c]);
+    vn[c] = (vrow && fv) ? sv[c] : 0.0f;
   }
 
   // a3: fluxes of row L-1 and etan(L-1)
-  float fx[C], fy[C], et[C];
+  float hx[C], hy[C], fx[C], fy[C], et[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    fx[c] = flux(w.un[c], w.h[c], (c < C - 1) ? w.h[c + 1] : w.hR);
-    fy[c] = flux(vn[c], w.h[c], hL[c]);
+    hx[c] = w.un[c] > 0.0f ? w.h[c] : ((c < C - 1) ? w.h[c + 1] : w.hR);
+    hy[c] = vn[c] > 0.0f ? w.h[c] : hL[c];
   }
+  vmul<C>(fx, w.un, hx);
+  vmul<C>(fy, vn, hy);
   const float fxw = __shfl_up_sync(kFull, fx[C - 1], 1);
+  float fw[C], t[C], t2[C];
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    const float fw = (c > 0) ? fx[c - 1] : fxw;
-    et[c] = __fsub_rn(__fsub_rn(w.e[c], __fmul_rn(x.cx, __fsub_rn(fx[c], fw))),
-                      __fmul_rn(x.cy, __fsub_rn(fy[c], w.fy[c])));
-  }
+  for (int c = 0; c < C; ++c) fw[c] = (c > 0) ? fx[c - 1] : fxw;
+  vsub<C>(t, fx, fw);
+  vmul<C>(t, x.cx, t);
+  vsub<C>(t, w.e, t);
+  vsub<C>(t2, fy, w.fy);
+  vmul<C>(t2, x.cy, t2);
+  vsub<C>(et, t, t2);
 
   // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
-  float En[C];
+  float En[C], t3[C];
+  vmul<C>(t3, w.w1, et);
+  vadd<C>(t3, t3, w.sS);
+  vmul<C>(t3, x.q, t3);
+  vadd<C>(t3, w.A, t3);
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    const float t3 = __fmul_rn(x.q, __fadd_rn(__fmul_rn(w.w1[c], et[c]), w.sS[c]));
-    En[c] = (w.w2[c] != 0.0f) ? __fadd_rn(w.A[c], t3) : w.etC[c];
-  }
+  for (int c = 0; c < C; ++c) En[c] = (w.w2[c] != 0.0f) ? t3[c] : w.etC[c];
 
   // a4 (first half) for row L-1: s, t1, t2, sS
   const float etW = __shfl_up_sync(kFull, et[C - 1], 1);
   const float etE = __shfl_down_sync(kFull, et[0], 1);
+  float wE[C], wW[C], eE[C], eW[C], sc[C], t1[C], xE[C], xW[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) {
-    const float wE = (c < C - 1) ? w.w1[c + 1] : w.w1E;
-    const float wW = (c > 0) ? w.w1[c - 1] : w.w1W;
-    const float s = __fadd_rn(__fadd_rn(__fadd_rn(wE, wW), wL[c]), w.w2[c]);
-    const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(x.q, s)), et[c]);
-    const float xE = __fmul_rn(wE, (c < C - 1) ? et[c + 1] : etE);
-    const float xW = __fmul_rn(wW, (c > 0) ? et[c - 1] : etW);
-    o.A[c] = __fadd_rn(t1, __fmul_rn(x.q, __fadd_rn(xE, xW)));
-    o.sS[c] = __fmul_rn(w.w2[c], w.etC[c]);
+    wE[c] = (c < C - 1) ? w.w1[c + 1] : w.w1E;
+    wW[c] = (c > 0) ? w.w1[c - 1] : w.w1W;
+    eE[c] = (c < C - 1) ? et[c + 1] : etE;
+    eW[c] = (c > 0) ? et[c - 1] : etW;
   }
+  vadd<C>(sc, wE, wW);
+  vadd<C>(sc, sc, wL);
+  vadd<C>(sc, sc, w.w2);
+  vmul<C>(sc, x.q, sc);
+  vsub<C>(sc, 1.0f, sc);
+  vmul<C>(t1, sc, et);
+  vmul<C>(xE, wE, eE);
+  vmul<C>(xW, wW, eW);
+  vadd<C>(xE, xE, xW);
+  vmul<C>(xE, x.q, xE);
+  vadd<C>(o.A, t1, xE);
+  vmul<C>(o.sS, w.w2, w.etC);
 
   // a5: commit (lanes 1..30, rows of this segment)
   if (x.out_lane) {
