@@ -361,6 +361,12 @@ __device__ __forceinline__ bool face_flow(bool wc, bool wn, float d) {
 #ifndef SW2D_F32X2
 #define SW2D_F32X2 1
 #endif
+// the step kernels pack only in the instantiations with diagnostics RED >=
+// SW2D_F32X2_MIN_RED (without diagnostics the packed form
+// measured slower on C3 and p2000)
+#ifndef SW2D_F32X2_MIN_RED
+#define SW2D_F32X2_MIN_RED 1
+#endif
 #define SW2D_PAIR_ASM(PTXOP)                                                                 \
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t" PTXOP      \
       " rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"                                                 \
@@ -381,22 +387,22 @@ __device__ __forceinline__ void vmul2(float& d0, float& d1, float a0, float a1, 
 }
 #undef SW2D_PAIR_ASM
 #define SW2D_PAIR_OP(NAME, SCALAR)                                                          \
-  template <int C>                                                                           \
+  template <int C, bool P = true>                                                            \
   __device__ __forceinline__ void NAME(float (&d)[C], const float (&a)[C],                   \
                                        const float (&b)[C]) {                                \
-    _Pragma("unroll") for (int c = 0; c < C; c += (SW2D_F32X2 ? 2 : 1)) {                    \
-      if (SW2D_F32X2 && c + 1 < C) {                                                         \
+    _Pragma("unroll") for (int c = 0; c < C; c += ((SW2D_F32X2 && P) ? 2 : 1)) {             \
+      if (SW2D_F32X2 && P && c + 1 < C) {                                                    \
         NAME##2(d[c], d[c + 1], a[c], a[c + 1], b[c], b[c + 1]);                             \
       } else {                                                                               \
         d[c] = SCALAR(a[c], b[c]);                                                           \
       }                                                                                      \
     }                                                                                        \
   }                                                                                          \
-  template <int C>                                                                           \
+  template <int C, bool P = true>                                                            \
   __device__ __forceinline__ void NAME(float (&d)[C], const float a, const float (&b)[C]) {  \
     float aa[C];                                                                             \
     _Pragma("unroll") for (int c = 0; c < C; ++c) aa[c] = a;                                 \
-    NAME<C>(d, aa, b);                                                                       \
+    NAME<C, P>(d, aa, b);                                                                    \
   }
 SW2D_PAIR_OP(vadd, __fadd_rn)
 SW2D_PAIR_OP(vsub, __fsub_rn)
@@ -439,9 +445,10 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
 
   // a1: h and wet flags of row L (rows outside 1..ny and columns outside
   // 1..nx are dry)
+  constexpr bool kPack = RED >= SW2D_F32X2_MIN_RED;
   const bool rowok = in_rows(L, 1, x.ny);
   float hL[C], wL[C];
-  vadd<C>(hL, h0L, eL);
+  vadd<C, kPack>(hL, h0L, eL);
 #pragma unroll
   for (int c = 0; c < C; ++c) wL[c] = (rowok && !(hL[c] < x.hmin)) ? x.cmf[c] : 0.0f;
   const float eR = __shfl_down_sync(kFull, eL[0], 1);
@@ -463,15 +470,15 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float en[C], du[C], dv[C], su[C], sv[C], un[C], vn[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) en[c] = (c < C - 1) ? eL[c + 1] : eR;
-  vsub<C>(du, en, eL);
+  vsub<C, kPack>(du, en, eL);
   float cg[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) cg[c] = x.cgxc[c];
-  vmul<C>(du, cg, du);
-  vsub<C>(dv, eL, w.e);
-  vmul<C>(dv, x.cgy, dv);
-  vadd<C>(su, uL, du);
-  vadd<C>(sv, w.v, dv);
+  vmul<C, kPack>(du, cg, du);
+  vsub<C, kPack>(dv, eL, w.e);
+  vmul<C, kPack>(dv, x.cgy, dv);
+  vadd<C, kPack>(su, uL, du);
+  vadd<C, kPack>(sv, w.v, dv);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float wn = (c < C - 1) ? wL[c + 1] : wR;
@@ -487,25 +494,25 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     hx[c] = w.un[c] > 0.0f ? w.h[c] : ((c < C - 1) ? w.h[c + 1] : w.hR);
     hy[c] = vn[c] > 0.0f ? w.h[c] : hL[c];
   }
-  vmul<C>(fx, w.un, hx);
-  vmul<C>(fy, vn, hy);
+  vmul<C, kPack>(fx, w.un, hx);
+  vmul<C, kPack>(fy, vn, hy);
   const float fxw = __shfl_up_sync(kFull, fx[C - 1], 1);
   float fw[C], t[C], t2[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) fw[c] = (c > 0) ? fx[c - 1] : fxw;
-  vsub<C>(t, fx, fw);
-  vmul<C>(t, x.cx, t);
-  vsub<C>(t, w.e, t);
-  vsub<C>(t2, fy, w.fy);
-  vmul<C>(t2, x.cy, t2);
-  vsub<C>(et, t, t2);
+  vsub<C, kPack>(t, fx, fw);
+  vmul<C, kPack>(t, x.cx, t);
+  vsub<C, kPack>(t, w.e, t);
+  vsub<C, kPack>(t2, fy, w.fy);
+  vmul<C, kPack>(t2, x.cy, t2);
+  vsub<C, kPack>(et, t, t2);
 
   // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
   float En[C], t3[C];
-  vmul<C>(t3, w.w1, et);
-  vadd<C>(t3, t3, w.sS);
-  vmul<C>(t3, x.q, t3);
-  vadd<C>(t3, w.A, t3);
+  vmul<C, kPack>(t3, w.w1, et);
+  vadd<C, kPack>(t3, t3, w.sS);
+  vmul<C, kPack>(t3, x.q, t3);
+  vadd<C, kPack>(t3, w.A, t3);
 #pragma unroll
   for (int c = 0; c < C; ++c) En[c] = (w.w2[c] != 0.0f) ? t3[c] : w.etC[c];
 
@@ -520,18 +527,18 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     eE[c] = (c < C - 1) ? et[c + 1] : etE;
     eW[c] = (c > 0) ? et[c - 1] : etW;
   }
-  vadd<C>(sc, wE, wW);
-  vadd<C>(sc, sc, wL);
-  vadd<C>(sc, sc, w.w2);
-  vmul<C>(sc, x.q, sc);
-  vsub<C>(sc, 1.0f, sc);
-  vmul<C>(t1, sc, et);
-  vmul<C>(xE, wE, eE);
-  vmul<C>(xW, wW, eW);
-  vadd<C>(xE, xE, xW);
-  vmul<C>(xE, x.q, xE);
-  vadd<C>(o.A, t1, xE);
-  vmul<C>(o.sS, w.w2, w.etC);
+  vadd<C, kPack>(sc, wE, wW);
+  vadd<C, kPack>(sc, sc, wL);
+  vadd<C, kPack>(sc, sc, w.w2);
+  vmul<C, kPack>(sc, x.q, sc);
+  vsub<C, kPack>(sc, 1.0f, sc);
+  vmul<C, kPack>(t1, sc, et);
+  vmul<C, kPack>(xE, wE, eE);
+  vmul<C, kPack>(xW, wW, eW);
+  vadd<C, kPack>(xE, xE, xW);
+  vmul<C, kPack>(xE, x.q, xE);
+  vadd<C, kPack>(o.A, t1, xE);
+  vmul<C, kPack>(o.sS, w.w2, w.etC);
 
   // a5: commit (lanes 1..30, rows of this segment)
   if (x.out_lane) {
