@@ -45,7 +45,24 @@ def test_built_for_sm100a(lib):
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("ny,p", [(10, 1), (17, 2), (100, 3), (16384 * 8, 8), (16, 2)])
+def test_step_kernels_have_no_fused_multiply_add(lib):
+    """Bitwise parity needs every product rounded before its add (DESIGN.md
+    §7, packed FP32 adds): ptxas 12.9 contracts a packed f32x2 mul feeding a
+    packed add into FFMA2 even under --fmad=false, so check the SASS of the
+    2DSW step kernels for any FFMA / FFMA2."""
+    import subprocess
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", sw2d._LIB_PATH],
+                          capture_output=True, text=True).stdout
+    funcs = re.split(r"\n\s+Function : ", sass)[1:]
+    steps = [f for f in funcs if "sw2d_step" in f.split("\n", 1)[0]]
+    assert steps, "no sw2d_step kernels found in the SASS"
+    for f in steps:
+        name = f.split("\n", 1)[0].strip()
+        assert not re.search(r"\bFFMA2?\b", f), f"fused multiply-add in {name}"
+    assert any(re.search(r"\bFADD2\b", f) for f in steps), "packed adds missing"
+
+
+@pytest.mark.parametrize("ny,p",[(10, 1), (17, 2), (100, 3), (16384 * 8, 8), (16, 2)])
 def test_partition_balanced_and_covering(lib, ny, p):
     rows = [sw2d.sw2d_partition(ny, p, r) for r in range(p)]
     assert rows[0][0] == 0
