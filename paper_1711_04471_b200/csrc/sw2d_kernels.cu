@@ -367,6 +367,9 @@ __device__ __forceinline__ bool face_flow(bool wc, bool wn, float d) {
 #ifndef SW2D_F32X2_MIN_RED
 #define SW2D_F32X2_MIN_RED 1
 #endif
+#ifndef SW2D_F32X2_SHIFTED
+#define SW2D_F32X2_SHIFTED 0
+#endif
 #define SW2D_PAIR_ASM(PTXOP)                                                                 \
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t" PTXOP      \
       " rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"                                                 \
@@ -446,6 +449,8 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   // a1: h and wet flags of row L (rows outside 1..ny and columns outside
   // 1..nx are dry)
   constexpr bool kPack = RED >= SW2D_F32X2_MIN_RED;
+  // the pairs with a neighbour-shifted operand (they need IMAD.MOV to align)
+  constexpr bool kPackS = kPack && SW2D_F32X2_SHIFTED;
   const bool rowok = in_rows(L, 1, x.ny);
   float hL[C], wL[C];
   vadd<C, kPack>(hL, h0L, eL);
@@ -470,7 +475,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float en[C], du[C], dv[C], su[C], sv[C], un[C], vn[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) en[c] = (c < C - 1) ? eL[c + 1] : eR;
-  vsub<C, kPack>(du, en, eL);
+  vsub<C, kPackS>(du, en, eL);
   float cg[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) cg[c] = x.cgxc[c];
@@ -500,7 +505,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float fw[C], t[C], t2[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) fw[c] = (c > 0) ? fx[c - 1] : fxw;
-  vsub<C, kPack>(t, fx, fw);
+  vsub<C, kPackS>(t, fx, fw);
   vmul<C, kPack>(t, x.cx, t);
   vsub<C, kPack>(t, w.e, t);
   vsub<C, kPack>(t2, fy, w.fy);
@@ -527,7 +532,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     eE[c] = (c < C - 1) ? et[c + 1] : etE;
     eW[c] = (c > 0) ? et[c - 1] : etW;
   }
-  vadd<C, kPack>(sc, wE, wW);
+  vadd<C, kPackS>(sc, wE, wW);
   vadd<C, kPack>(sc, sc, wL);
   vadd<C, kPack>(sc, sc, w.w2);
   vmul<C, kPack>(sc, x.q, sc);
