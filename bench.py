@@ -106,12 +106,13 @@ def ncu_traffic(workload, kernel):
     return d.get("dram_bytes_per_launch")
 
 
-def ncu_instr_per_cell_step(kernel):
-    for w in _ncu_summary().values():
-        d = w.get(kernel, {})
-        if "thread_instr_per_cell_step" in d:
-            return d["thread_instr_per_cell_step"]
-    return None
+def ncu_instr_per_cell_step(workload, kernel):
+    """Thread-instructions per cell-step of `kernel` on `workload` from the
+    committed ncu capture, with the capture's name, or (None, None)."""
+    d = _ncu_summary().get(workload, {}).get(kernel, {})
+    if "thread_instr_per_cell_step" in d:
+        return d["thread_instr_per_cell_step"], d.get("capture", "profiles/ncu_summary.json")
+    return None, None
 
 
 def max_sm_mhz():
@@ -375,29 +376,38 @@ def run_ours(args, cfg, ws, rank, local):
             kname = "sw2d_step_cta<%d, 0>" % red_lvl
         if args.variant != "fused":
             kname = "paper_momentum + paper_continuity + paper_shapiro_update (per step)"
-        hbm = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s",
-               "frac": hbm_achieved / peak, "peak_source": peak_src,
-               "traffic": ncu_traffic(cfg["name"], kname) if args.variant == "fused" else None,
-               "algorithmic_bytes_per_launch": alg_bytes, "model_steps_per_launch": spl}
-        roof = dict(hbm, kernel=kname, launches_per_model_step=launches_per_step,
-                    plan=sw2d.sw2d_plan(h))
-        ipc = ncu_instr_per_cell_step(kname)
-        if spl == 2 and ipc:
-            # two steps per launch move 14 B per cell-step: the launch is bound by
-            # instruction issue: 4 warp-instr/clk/SM x 32
-            # lanes x SMs x max SM clock
+        # The binding ceiling is HBM: a launch moves the state once in and once
+        # out (28 B/cell) whatever number of model steps it advances, i.e. 14
+        # B/cell-step for the two-step kernel.  `achieved` =
+        # those bytes / the launch's average duration, from the CUDA events
+        # around the timed region (the handle's stream) divided by the
+        # launches in it (the graphs' tiny set_dstep / ring_scatter kernels
+        # included, so it slightly understates the step kernel).
+        roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": peak, "unit": "GB/s",
+                "frac": hbm_achieved / peak, "peak_source": peak_src,
+                "traffic": ncu_traffic(cfg["name"], kname) if args.variant == "fused" else None,
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "algorithmic_bytes_per_cell_step": bpc / spl, "model_steps_per_launch": spl,
+                "kernel": kname, "launches_per_model_step": launches_per_step,
+                "plan": sw2d.sw2d_plan(h)}
+        # the survey's single-step budget (28 B per cell-STEP):
+        # above 1 here because two steps share one HBM pass
+        roof["survey_28B_frac"] = value / ws * BYTES_PER_CELL / 1e9 / peak
+        ipc, ipc_src = ncu_instr_per_cell_step(cfg["name"], kname)
+        if ipc:
+            # the other ceiling: instruction issue, 4 warp-instr/clk/SM x 32
+            # lanes x SMs x max SM clock, at ncu's thread-instructions per
+            # cell-step for this kernel on this workload
             sm_hz = max_sm_mhz() * 1e6
             sms = torch.cuda.get_device_properties(local).multi_processor_count
             issue_peak = 4 * 32 * sms * sm_hz / 1e12
             ach = ipc * (cells_local * spl / t_launch_s) / 1e12
-            roof = {"bound": "alu", "achieved": ach, "peak": issue_peak, "unit": "Tinstr/s",
-                    "frac": ach / issue_peak, "traffic": hbm["traffic"], "kernel": kname,
-                    "thread_instr_per_cell_step": ipc,
-                    "peak_source": "4 warp-instructions/clk/SM x 32 x %d SMs x %.0f MHz "
-                                   "(B200_PROFILING.md / B300_MICROARCH.md issue model)"
-                                   % (sms, sm_hz / 1e6),
-                    "launches_per_model_step": launches_per_step, "hbm_view": hbm,
-                    "plan": sw2d.sw2d_plan(h)}
+            roof["issue_view"] = {
+                "bound": "alu", "achieved": ach, "peak": issue_peak, "unit": "Tinstr/s",
+                "frac": ach / issue_peak, "thread_instr_per_cell_step": ipc, "ncu": ipc_src,
+                "peak_source": "4 warp-instructions/clk/SM x 32 x %d SMs x %.0f MHz "
+                               "(B200_PROFILING.md / B300_MICROARCH.md issue model)"
+                               % (sms, sm_hz / 1e6)}
 
         # --- periodic output overlapped with compute (optional) ------------
         snaps = None
@@ -417,85 +427,115 @@ def run_ours(args, cfg, ws, rank, local):
                      "path": "sw2d_run_snapshots(T, every=T) per bench step, pinned host"}
 
         # --- e2e: host buffers through the C ABI ----------------------------
-        # Every bench step uploads its inputs from pinned host memory
-        # (sw2d_set_state), runs sw2d_step(T) and reads the step's VOLUME
-        # history back.  One GPU: two handles on two streams, double-buffered
-        # the way a user runs a stream of independent problems — step k+1's
-        # upload (a blocking call) proceeds while step k computes; the steps
-        # themselves are serialised (an event), so compute never overlaps
-        # compute and e2e cannot exceed the device-resident value.  Several
-        # ranks: one handle, serial (a second NCCL communicator per rank is
-        # not worth the risk here).  The serial figure is reported as well.
+        # Every bench step is one independent problem through the public API:
+        # sw2d_set_state from pinned host memory (16 B/cell H2D), sw2d_step(T),
+        # then the result back to pinned host memory — the state eta, u, v
+        # (sw2d_get_state, 12 B/cell D2H) and the T per-step volumes
+        # (sw2d_reduce_history).  Wall clock around the whole loop, synchronized
+        # on both sides.  One GPU: three handles on three streams, pipelined
+        # the way a user runs a stream of problems — problem k+1 uploads and
+        # problem k-1 downloads (two host threads; the calls block) while
+        # problem k computes; the computes are serialised by events, so
+        # compute never overlaps compute.  Several ranks: one handle, serial.
         e2e = None
         if not args.no_e2e and not args.profile:
-            def read_back(hh, out):
-                if mask:
-                    sw2d.sw2d_reduce_history(hh, sw2d.SW2D_RED_VOLUME, T, out)
-                else:
-                    sw2d.sw2d_reduce(hh, sw2d.SW2D_RED_VOLUME)
+            out_state = [[torch.empty((nrows, nx), dtype=torch.float32, pin_memory=True)
+                          for _ in range(3)] for _ in range(3)]
+            out_hist = [np.empty(max(T, 1), np.float64) for _ in range(3)]
 
-            hist = np.empty(T, np.float64)
+            def read_back(hh, b):
+                sw2d.sw2d_get_state(hh, *out_state[b])
+                if mask:
+                    sw2d.sw2d_reduce_history(hh, sw2d.SW2D_RED_VOLUME, T, out_hist[b])
+                else:
+                    out_hist[b][0] = sw2d.sw2d_reduce(hh, sw2d.SW2D_RED_VOLUME)
+
             barrier()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             t0 = time.perf_counter()
-            e0.record(stream)
             for _ in range(args.steps):
                 sw2d.sw2d_set_state(h, *host)
                 sw2d.sw2d_step(h, T)
-                read_back(h, hist)
-            e1.record(stream)
+                read_back(h, 0)
             sw2d.sw2d_sync(h)
             torch.cuda.synchronize()
-            wall_serial = time.perf_counter() - t0
+            wall_serial = max_over_ranks(time.perf_counter() - t0)
             barrier()
-            ems_serial = max_over_ranks(e0.elapsed_time(e1))
-            ems, wall, how = ems_serial, wall_serial, "serial, one handle"
+            ref_eta = out_state[0][0].clone()
+            wall, how = wall_serial, "serial, one handle"
             if ws == 1:
-                stream2 = torch.cuda.Stream()
-                h2 = sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid, halo), stream2)
+                import threading
+                nh = 3
+                streams = [stream] + [torch.cuda.Stream() for _ in range(nh - 1)]
+                hs = [h] + [sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid, halo), st)
+                            for st in streams[1:]]
                 try:
-                    hs = (h, h2)
-                    hist2 = [np.empty(T, np.float64), np.empty(T, np.float64)]
-                    sw2d.sw2d_set_state(h2, *host)   # warm the second handle (graphs, plan)
-                    sw2d.sw2d_step(h2, T)
-                    sw2d.sw2d_sync(h2)
+                    for hh in hs[1:]:   # warm the other handles (graphs, plan)
+                        sw2d.sw2d_set_state(hh, *host)
+                        sw2d.sw2d_step(hh, T)
+                        sw2d.sw2d_sync(hh)
                     torch.cuda.synchronize()
-                    ev2 = torch.cuda.Event()
-                    strs = (stream, stream2)
-                    done = [torch.cuda.Event(), torch.cuda.Event()]
+                    done = [torch.cuda.Event() for _ in range(args.steps)]
+                    enq = [threading.Event() for _ in range(args.steps)]
+                    freed = [threading.Event() for _ in range(args.steps)]
+                    err = []
+
+                    def uploader():
+                        try:
+                            for k in range(args.steps):
+                                b = k % nh
+                                if k >= nh:
+                                    freed[k - nh].wait()
+                                sw2d.sw2d_set_state(hs[b], *host)
+                                if k > 0:   # computes run one after another
+                                    streams[b].wait_event(done[k - 1])
+                                sw2d.sw2d_step(hs[b], T)
+                                done[k].record(streams[b])
+                                enq[k].set()
+                        except Exception as ex:   # surface in the main thread
+                            err.append(ex)
+                            for e_ in enq:
+                                e_.set()
+
+                    def downloader():
+                        try:
+                            for k in range(args.steps):
+                                enq[k].wait()
+                                if err:
+                                    return
+                                read_back(hs[k % nh], k % nh)
+                                freed[k].set()
+                        except Exception as ex:
+                            err.append(ex)
+                            for f_ in freed:
+                                f_.set()
+
                     t0 = time.perf_counter()
-                    e0.record(stream)
-                    stream2.wait_event(e0)
-                    for k in range(args.steps):
-                        cur = hs[k % 2]
-                        sw2d.sw2d_set_state(cur, *host)   # overlaps the other handle's step
-                        if k > 0:   # only uploads overlap: the steps run one after another
-                            strs[k % 2].wait_event(done[(k - 1) % 2])
-                        sw2d.sw2d_step(cur, T)
-                        done[k % 2].record(strs[k % 2])
-                        if k > 0:
-                            read_back(hs[(k - 1) % 2], hist2[(k - 1) % 2])
-                    read_back(hs[(args.steps - 1) % 2], hist2[(args.steps - 1) % 2])
-                    ev2.record(stream2)
-                    stream.wait_event(ev2)
-                    e1.record(stream)
+                    th = [threading.Thread(target=uploader), threading.Thread(target=downloader)]
+                    for t_ in th:
+                        t_.start()
+                    for t_ in th:
+                        t_.join()
                     torch.cuda.synchronize()
                     wall = time.perf_counter() - t0
-                    ems = e0.elapsed_time(e1)
-                    how = "double-buffered, two handles on two streams"
-                    assert np.array_equal(hist2[(args.steps - 1) % 2], hist) or not mask, \
-                        "e2e: the two handles disagree"
+                    if err:
+                        raise err[0]
+                    how = "pipelined: three handles on three streams, upload / compute / download"
+                    last = (args.steps - 1) % nh
+                    assert torch.equal(out_state[last][0], ref_eta), "e2e: handles disagree"
                 finally:
-                    sw2d.sw2d_destroy(h2)
-            e2e = {"value": nx * ny * T * args.steps / (ems * 1e-3), "unit": UNIT,
+                    for hh in hs[1:]:
+                        sw2d.sw2d_destroy(hh)
+            e2e = {"value": nx * ny * T * args.steps / wall, "unit": UNIT,
                    "h2d_bytes_per_step": 16 * cells_local,
-                   "d2h_bytes_per_step": 8 * T if mask else 8,
-                   "ms_per_step": ems / args.steps, "wall_s": wall,
-                   "path": "sw2d_set_state(pinned host) + sw2d_step(T) + "
-                           "sw2d_reduce_history(VOLUME, T) per bench step; " + how,
-                   "serial": {"value": nx * ny * T * args.steps / (ems_serial * 1e-3),
-                              "ms_per_step": ems_serial / args.steps, "wall_s": wall_serial}}
+                   "d2h_bytes_per_step": 12 * cells_local + (8 * T if mask else 8),
+                   "ms_per_step": 1e3 * wall / args.steps, "wall_s": wall,
+                   "path": "sw2d_set_state(pinned host hzero, eta, u, v) + sw2d_step(T) + "
+                           "sw2d_get_state(pinned host eta, u, v) + sw2d_reduce_history(VOLUME, "
+                           "T) per bench step, wall clock; " + how,
+                   "serial": {"value": nx * ny * T * args.steps / wall_serial,
+                              "ms_per_step": 1e3 * wall_serial / args.steps,
+                              "wall_s": wall_serial}}
     finally:
         sw2d.sw2d_destroy(h)
 

@@ -40,13 +40,14 @@
 #ifndef SW2D_H
 #define SW2D_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define SW2D_ABI_VERSION 3
+#define SW2D_ABI_VERSION 4
 
 /* Halo depth (rows) of a row slab: the dependency cone of a two-step pass. */
 #define SW2D_HALO_ROWS 4
@@ -107,7 +108,24 @@ enum {
   SW2D_HALO_P2P = 1   /* fused: the boundary launch of each step stores its rows
                          straight into the neighbours' halo rows (peer memory over
                          NVLink via CUDA IPC; another slab's buffers for virtual
-                         ranks) and signals them with stream memory operations   */
+                         ranks) and signals them with stream memory operations.
+                         Per-step diagnostics are exchanged the same way: every
+                         rank stores its partial record into a slot of every
+                         peer and each rank folds the slots in rank order
+                         (deterministic, bitwise identical on every rank; no
+                         NCCL on the data path)                                  */
+};
+
+/* How the ranks of a real multi-rank run find each other (sw2d_dist.bootstrap). */
+enum {
+  SW2D_BOOT_NCCL = 0,    /* an NCCL communicator from nccl_id (required by
+                            SW2D_HALO_NCCL; with SW2D_HALO_P2P it only carries the
+                            one-time all-gather of the peer blobs at create)      */
+  SW2D_BOOT_EXTERNAL = 1 /* no NCCL at all (SW2D_HALO_P2P only): after create the
+                            caller all-gathers every rank's sw2d_p2p_export blob
+                            (e.g. over gloo) and passes them to sw2d_p2p_import
+                            before sw2d_set_state.  Ranks may share one GPU
+                            (CUDA IPC within a device) or sit on peer GPUs      */
 };
 
 typedef struct {
@@ -118,7 +136,9 @@ typedef struct {
                             handle then owns the whole grid (test mode)          */
   int32_t halo_mode;     /* SW2D_HALO_*                                           */
   unsigned char nccl_id[128]; /* ncclUniqueId from rank 0 (sw2d_nccl_unique_id),
-                                 broadcast by the caller (e.g. torch.distributed) */
+                                 broadcast by the caller (e.g. torch.distributed);
+                                 unused with SW2D_BOOT_EXTERNAL                   */
+  int32_t bootstrap;     /* SW2D_BOOT_* (real ranks only)                         */
 } sw2d_dist;
 
 /* Library ABI version (SW2D_ABI_VERSION of the built library). */
@@ -148,6 +168,9 @@ int sw2d_halo_plan(int64_t ny, int32_t nranks, int32_t rank, int64_t out[4]);
  * SW2D_ENCCL if NCCL cannot be loaded. */
 int sw2d_nccl_unique_id(unsigned char out[128]);
 
+/* Bytes of one rank's peer blob (sw2d_p2p_export / sw2d_p2p_import). */
+#define SW2D_P2P_BLOB_BYTES 1024
+
 /* Create a handle.  dist == NULL: one GPU (the current device), whole grid.
  * cuda_stream: a cudaStream_t to enqueue on (e.g. torch's current stream), or
  * NULL for a library-owned stream.  Allocates 7 device arrays (hzero and
@@ -156,8 +179,31 @@ int sw2d_nccl_unique_id(unsigned char out[128]);
 int sw2d_create(const sw2d_params* params, const sw2d_dist* dist,
                 void* cuda_stream, sw2d** out);
 
+/* P2P mode across real ranks (SW2D_HALO_P2P; SURVEY.md §8(e) "Fused P2P
+ * alternative"): write this rank's peer blob — its grid geometry and the CUDA
+ * IPC handles of its state buffers (eta, u, v double-buffered, hzero) and of
+ * its sync buffer (halo flags, the record-exchange flags and slots) — into
+ * out[0 .. SW2D_P2P_BLOB_BYTES).  The blob is plain bytes: the caller moves it
+ * to every rank (any transport).  SW2D_EINVAL if the handle is not a real
+ * rank in P2P mode. */
+int sw2d_p2p_export(sw2d* h, void* out, size_t cap);
+
+/* Map the peers: `blobs` holds nranks blobs of SW2D_P2P_BLOB_BYTES each, in
+ * rank order (rank r's own blob at r, as exported).  Opens the row
+ * neighbours' state buffers and every peer's sync buffer (CUDA IPC; peer GPUs
+ * over NVLink with lazy peer access, or the same GPU).  Checks that every
+ * blob describes the same grid and partition (SW2D_EINVAL otherwise).  Call
+ * once, after create and before sw2d_set_state, on every rank (with
+ * SW2D_BOOT_NCCL, create has already done it). */
+int sw2d_p2p_import(sw2d* h, const void* blobs, size_t nbytes);
+
 /* Rows [*j0, *j0 + *nrows) (0-based, global) whose state this handle holds. */
 int sw2d_local_rows(const sw2d* h, int64_t* j0, int64_t* nrows);
+
+/* Shape of the host-visible [nrows][nx] arrays of this handle (the rows of
+ * sw2d_local_rows, the global nx): what set_state reads and get_state writes
+ * per field. */
+int sw2d_local_shape(const sw2d* h, int64_t* nrows, int64_t* nx);
 
 /* Upload the state (the paper's once-per-run write-buffer): hzero, eta, u, v
  * as [nrows][nx] float32 (see layout above).  u and v may be NULL (= 0).
@@ -172,7 +218,10 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
  * kernels allow it, and long calls in one process replay CUDA graphs.  With
  * nranks > 1 it exchanges the SW2D_HALO_ROWS-row halos before every pass of
  * one or two steps (NCCL send/recv, or fused P2P stores) and, if
- * reduce_every_step != 0, allreduces the per-step diagnostics. */
+ * reduce_every_step != 0, combines the per-step diagnostics of all ranks
+ * (NCCL allreduce, or the P2P slot exchange) into every rank's history.
+ * Every rank must make the same sequence of sw2d_set_state / sw2d_step /
+ * sw2d_reduce calls (collective). */
 int sw2d_step(sw2d* h, int64_t nsteps);
 
 /* Periodic output (the paper's once-per-run / per-iteration transfer

@@ -63,12 +63,30 @@ def build(force: bool = False, verbose: bool = False, extra=(), debug: bool = Fa
     elif not force and not _stale():
         return LIB
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-I", _nccl_include(), *sources(), "-o", tmp, "-ldl"]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
-    os.replace(tmp, out)
+    objdir = out + f".obj{os.getpid()}"
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", _nccl_include()]
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    jobs = []
+    for src in sources():   # one nvcc per translation unit, in parallel, then link
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        jobs.append([NVCC, *compile_flags, *extra, *inc, "-c", src, "-o", obj])
+    try:
+        procs = []
+        for cmd in jobs:
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            procs.append((cmd, subprocess.Popen(cmd)))
+        for cmd, pr in procs:
+            if pr.wait() != 0:
+                raise subprocess.CalledProcessError(pr.returncode, cmd)
+        link = [NVCC, *FLAGS, *extra, *[c[-1] for c in jobs], "-o", tmp, "-ldl"]
+        subprocess.check_call(link)
+        os.replace(tmp, out)
+    finally:
+        for f in glob.glob(os.path.join(objdir, "*.o")):
+            os.remove(f)
+        os.rmdir(objdir)
     return out
 
 

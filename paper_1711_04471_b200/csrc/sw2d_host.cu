@@ -62,7 +62,8 @@ struct sw2d {
   sw2d_params p{};
   Coef coef{};
   int rank = 0, nranks = 1;
-  bool virt = false, multi = false;  // multi: real ranks with NCCL
+  bool virt = false, multi = false;  // multi: real ranks (NCCL or P2P transport)
+  int bootstrap = SW2D_BOOT_NCCL;    // real ranks: SW2D_BOOT_*
   int device = 0;
   int64_t pitch = 0;
   int nstrips = 0;
@@ -107,7 +108,26 @@ struct sw2d {
   int64_t steps = 0;
   int wcur = 0;  // paper variant: current wet buffer
   bool state_set = false;
-  std::vector<int64_t> pending;  // steps whose diagnostics await the allreduce (NCCL mode)
+  // records of real ranks: each pass's kernels write this rank's partial
+  // record of exchange sequence number q to its own slot xslot[q % kXRing]
+  // [rank] of the sync buffer; the comm stream combines the ranks' slots into
+  // the destination (history slot or scratch): NCCL allreduce (out of place),
+  // or in P2P mode the slot exchange (every rank stores its record into every
+  // peer's slot, each folds in rank order).  ev_x[q % kXRing] is recorded on
+  // the comm stream once record q is combined; the compute stream waits on it
+  // before a kernel reuses the slot.
+  struct PendingRec {
+    uint64_t seq;
+    double* dst;
+  };
+  std::vector<PendingRec> pending;  // records awaiting the NCCL allreduce
+  uint64_t xseq = 0;                // records exchanged so far (never reset)
+  uint32_t hseq = 0;                // P2P halo signals sent to each neighbour (never reset)
+  unsigned char* sync = nullptr;    // flags + record slots (IPC-exported in P2P mode)
+  size_t sync_bytes = 0;
+  std::vector<unsigned char*> psync;  // every peer's sync buffer, IPC-mapped (P2P)
+  bool p2p_ready = false;           // P2P peers mapped (sw2d_p2p_import)
+  cudaEvent_t ev_x[64] = {};
   // CUDA graphs of kGraphPasses passes (one slab, no per-step diagnostics),
   // one per starting buffer parity; replayed for long sw2d_step calls
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -119,19 +139,79 @@ struct sw2d {
   int64_t nlaunch = 0;
   // P2P halo mode
   int halo_mode = SW2D_HALO_NCCL;
-  unsigned int* flags = nullptr;  // [0]: written by the south neighbour, [1]: by the north
   struct Peer {
     bool present = false;
     float* E[2] = {nullptr, nullptr};
     float* U[2] = {nullptr, nullptr};
     float* V[2] = {nullptr, nullptr};
-    unsigned int* flags = nullptr;
+    float* H0 = nullptr;
     long long jbase = 0;
     long long nelem = 0;
+    long long nrows = 0;
   } nbr[2];                       // [0]: south (rank-1), [1]: north (rank+1); IPC-mapped
 };
 
 namespace {
+
+// --- real ranks: the sync buffer --------------------------------------------
+// One device allocation per rank (IPC-exported in P2P mode), zeroed at create:
+//   bytes [0, 8)          halo flags: [0] written by the south neighbour, [1]
+//                         by the north one (P2P: halo signals received so far)
+//   bytes [64, 64+4P)     xflag[q]: records rank q has stored into this rank's slots
+//   bytes [.., +4P)       xack[q]:  records rank q has folded (its slots reusable)
+//   from sync_slots(P)    double slots[kXRing][P][kRecN]: record q of rank r at
+//                         [q % kXRing][r]
+// Flag values count events since create and are never reset (no epoch race
+// between a neighbour's last signal of one run and the next sw2d_set_state).
+constexpr int kXRing = 64;
+constexpr int kMaxRanks = 128;
+static_assert(kXRing == sizeof(((sw2d*)nullptr)->ev_x) / sizeof(cudaEvent_t), "ev_x size");
+size_t sync_xflag() { return 64; }
+size_t sync_xack(int P) { return 64 + 4 * (size_t)P; }
+size_t sync_slots(int P) { return (64 + 8 * (size_t)P + 255) / 256 * 256; }
+size_t sync_size(int P) { return sync_slots(P) + sizeof(double) * kRecN * kXRing * (size_t)P; }
+unsigned long long flag_addr(unsigned char* sync, size_t off, int i) {
+  return (unsigned long long)(sync + off + 4 * (size_t)i);
+}
+double* xslot(unsigned char* sync, int P, uint64_t seq, int r) {
+  return reinterpret_cast<double*>(sync + sync_slots(P)) +
+         ((size_t)(seq % kXRing) * (size_t)P + (size_t)r) * kRecN;
+}
+
+// P2P record exchange, step 1: this rank's records seq0 .. seq0+n-1 (its own
+// slots) are stored into the same slots of every peer's buffer.
+struct XPeers {
+  double* slots[kMaxRanks];  // each rank's slot array as mapped here (nullptr: self)
+};
+__global__ void xpush(const double* mine, XPeers peers, int P, int me, unsigned long long seq0,
+                      int n) {
+  const int per = n * kRecN;
+  for (int i = threadIdx.x; i < P * per; i += blockDim.x) {
+    const int q = i / per, k = (i % per) / kRecN, f = i % kRecN;
+    if (q == me || !peers.slots[q]) continue;
+    const size_t o = ((size_t)((seq0 + (unsigned long long)k) % kXRing) * (size_t)P + me) * kRecN + f;
+    peers.slots[q][o] = mine[o];
+  }
+}
+
+// step 2 (after every peer's signal): the global record of each of the n
+// records is the fold of the P ranks' slots in rank order — sums [0..2] added
+// 0 + 1 + ... + P-1 left to right, maxima [3..6] — so every rank computes the
+// bitwise same value ("each rank sums the slots in rank order").
+__global__ void xfold(const double* slots, int P, unsigned long long seq0, int n, double* dst0,
+                      double* dst1) {
+  const int t = threadIdx.x;
+  if (t >= n * kRecN) return;
+  const int k = t / kRecN, f = t % kRecN;
+  const volatile double* s =
+      slots + (size_t)((seq0 + (unsigned long long)k) % kXRing) * (size_t)P * kRecN + f;
+  double acc = s[0];
+  for (int q = 1; q < P; ++q) {
+    const double v = s[(size_t)q * kRecN];
+    acc = f < kRecMaxEta ? acc + v : fmax(acc, v);
+  }
+  (k ? dst1 : dst0)[f] = acc;
+}
 
 // NVTX range over an API call (visible in nsys / ncu timelines; ~free
 // without a tool attached)
@@ -563,13 +643,80 @@ int nccl_halo(sw2d* h, int b, cudaStream_t st) {
   return SW2D_OK;
 }
 
-// In-place allreduce of a 7-double record: sums [0..2], maxima [3..6].
-int nccl_allreduce_rec(sw2d* h, double* rec, cudaStream_t st) {
+// Allreduce of a 7-double record (src -> dst, may alias): sums [0..2], maxima [3..6].
+int nccl_allreduce_rec(sw2d* h, const double* src, double* dst, cudaStream_t st) {
   const auto& nc = sw2d_host::nccl();
   NCCL_TRY(h, nc.GroupStart());
-  NCCL_TRY(h, nc.AllReduce(rec, rec, 3, ncclFloat64, ncclSum, h->comm_nccl, st));
-  NCCL_TRY(h, nc.AllReduce(rec + 3, rec + 3, 4, ncclFloat64, ncclMax, h->comm_nccl, st));
+  NCCL_TRY(h, nc.AllReduce(src, dst, 3, ncclFloat64, ncclSum, h->comm_nccl, st));
+  NCCL_TRY(h, nc.AllReduce(src + 3, dst + 3, 4, ncclFloat64, ncclMax, h->comm_nccl, st));
   NCCL_TRY(h, nc.GroupEnd());
+  return SW2D_OK;
+}
+
+// Before kernels write this rank's slots of records seq0 .. seq0+n-1 (compute
+// stream): the record that last used the newest of those slots has been
+// combined (its ev_x was recorded on the comm stream when it was enqueued —
+// at least kXRing - 2 records ago, so always recorded already).
+int guard_slots(sw2d* h, uint64_t seq0, int n) {
+  const uint64_t last = seq0 + (uint64_t)n - 1;
+  if (last >= (uint64_t)kXRing)
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_x[(last - kXRing) % kXRing], 0));
+  return SW2D_OK;
+}
+
+// NCCL mode: allreduce the pending records (slot -> destination) on the comm
+// stream, which has already waited for the pass that produced them.
+int flush_pending(sw2d* h) {
+  for (const sw2d::PendingRec& r : h->pending) {
+    int rc = nccl_allreduce_rec(h, xslot(h->sync, h->nranks, r.seq, h->rank), r.dst, h->comm);
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_x[r.seq % kXRing], h->comm));
+  }
+  h->pending.clear();
+  return SW2D_OK;
+}
+
+// P2P mode: combine records seq0 .. seq0+n-1 (n <= 2; this rank's parts are in
+// its own slots) into dst[k] on every rank, on the comm stream (which has
+// waited for the work that wrote the slots).  No NCCL: stream memory
+// operations order it, kernels move and fold the records.
+int p2p_exchange(sw2d* h, uint64_t seq0, int n, double* dst0, double* dst1) {
+  const auto& mo = sw2d_host::memops();
+  const int P = h->nranks, me = h->rank;
+  const uint64_t end = seq0 + (uint64_t)n;
+  // 1. every peer has folded the records whose slots these overwrite
+  if (end > (uint64_t)kXRing)
+    for (int q = 0; q < P; ++q)
+      if (q != me && mo.wait32(h->comm, flag_addr(h->sync, sync_xack(P), q),
+                               (unsigned)(end - kXRing), 0x0 /*GEQ*/))
+        return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
+  // 2. this rank's records into every peer's slots, then tell them
+  if (P > 1) {
+    XPeers xp{};
+    for (int q = 0; q < P; ++q)
+      xp.slots[q] = q == me ? nullptr : reinterpret_cast<double*>(h->psync[q] + sync_slots(P));
+    xpush<<<1, 128, 0, h->comm>>>(reinterpret_cast<const double*>(h->sync + sync_slots(P)), xp, P,
+                                  me, (unsigned long long)seq0, n);
+    h->nlaunch++;
+    CUDA_TRY(h, cudaGetLastError());
+  }
+  for (int q = 0; q < P; ++q)
+    if (q != me && mo.write32(h->comm, flag_addr(h->psync[q], sync_xflag(), me), (unsigned)end, 0x0))
+      return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
+  // 3. every peer's records have landed here
+  for (int q = 0; q < P; ++q)
+    if (q != me && mo.wait32(h->comm, flag_addr(h->sync, sync_xflag(), q), (unsigned)end, 0x0))
+      return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
+  // 4. fold in rank order; the slots are free again once the peers know
+  xfold<<<1, 32, 0, h->comm>>>(reinterpret_cast<const double*>(h->sync + sync_slots(P)), P,
+                               (unsigned long long)seq0, n, dst0, dst1);
+  h->nlaunch++;
+  CUDA_TRY(h, cudaGetLastError());
+  for (int k = 0; k < n; ++k)
+    CUDA_TRY(h, cudaEventRecord(h->ev_x[(seq0 + (uint64_t)k) % kXRing], h->comm));
+  for (int q = 0; q < P; ++q)
+    if (q != me && mo.write32(h->comm, flag_addr(h->psync[q], sync_xack(P), me), (unsigned)end, 0x0))
+      return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
   return SW2D_OK;
 }
 
@@ -621,65 +768,168 @@ void free_all(sw2d* h) {
   if (h->comm) cudaStreamDestroy(h->comm);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   for (auto& pr : h->nbr) {
-    if (!pr.present) continue;
     for (int b = 0; b < 2; ++b) {
       if (pr.E[b]) cudaIpcCloseMemHandle(pr.E[b]);
       if (pr.U[b]) cudaIpcCloseMemHandle(pr.U[b]);
       if (pr.V[b]) cudaIpcCloseMemHandle(pr.V[b]);
     }
-    if (pr.flags) cudaIpcCloseMemHandle(pr.flags);
+    if (pr.H0) cudaIpcCloseMemHandle(pr.H0);
+    pr = sw2d::Peer{};
   }
-  cudaFree(h->flags);
+  for (unsigned char*& q : h->psync) {
+    if (q) cudaIpcCloseMemHandle(q);
+    q = nullptr;
+  }
+  cudaFree(h->sync);
+  for (cudaEvent_t& e : h->ev_x)
+    if (e) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b)
     if (h->graph[b]) cudaGraphExecDestroy(h->graph[b]);
   if (h->comm_nccl && sw2d_host::nccl().ok) sw2d_host::nccl().CommDestroy(h->comm_nccl);
 }
 
-// P2P halo mode across real ranks: export this rank's six state buffers and
-// its flag words with CUDA IPC, all-gather the handles over NCCL, and map the
-// row neighbours' buffers (NVLink peer memory).
-int setup_p2p(sw2d* h) {
-  const auto& nc = sw2d_host::nccl();
+// P2P mode across real ranks: this rank's peer blob (sw2d_p2p_export) — the
+// geometry the importers check, and the CUDA IPC handles of its six state
+// buffers, hzero and the sync buffer.
+struct PeerBlob {
+  uint32_t magic, version;
+  int32_t rank, nranks;
+  int64_t nx, ny, pitch, j0, nrows;
+  int32_t xring, nhandles;
+  cudaIpcMemHandle_t mem[8];  // E0 E1 U0 U1 V0 V1 H0 sync
+};
+static_assert(sizeof(PeerBlob) <= SW2D_P2P_BLOB_BYTES, "blob size");
+constexpr uint32_t kBlobMagic = 0x50325753u;  // "SW2P"
+
+bool p2p_real(const sw2d* h) { return h->multi && h->halo_mode == SW2D_HALO_P2P; }
+
+int p2p_export(sw2d* h, unsigned char* out) {
+  if (!p2p_real(h)) return fail(h, SW2D_EINVAL, "sw2d_p2p_export: not a real rank in P2P mode");
+  std::memset(out, 0, SW2D_P2P_BLOB_BYTES);
+  PeerBlob b{};
+  const Slab& sl = h->slabs[0];
+  b.magic = kBlobMagic;
+  b.version = SW2D_ABI_VERSION;
+  b.rank = h->rank;
+  b.nranks = h->nranks;
+  b.nx = h->p.nx;
+  b.ny = h->p.ny;
+  b.pitch = h->pitch;
+  b.j0 = sl.j0;
+  b.nrows = sl.nrows;
+  b.xring = kXRing;
+  b.nhandles = 8;
+  void* mine[8] = {sl.E[0], sl.E[1], sl.U[0], sl.U[1], sl.V[0], sl.V[1], sl.H0, h->sync};
+  for (int i = 0; i < 8; ++i) CUDA_TRY(h, cudaIpcGetMemHandle(&b.mem[i], mine[i]));
+  std::memcpy(out, &b, sizeof(b));
+  return SW2D_OK;
+}
+
+// Map the peers from all ranks' blobs (rank order): the row neighbours' state
+// buffers and hzero (halo stores) and every peer's sync buffer (flags, slots).
+int p2p_import(sw2d* h, const unsigned char* blobs) {
+  if (!p2p_real(h)) return fail(h, SW2D_EINVAL, "sw2d_p2p_import: not a real rank in P2P mode");
+  if (h->p2p_ready) return fail(h, SW2D_EINVAL, "sw2d_p2p_import: peers already mapped");
   if (!sw2d_host::memops().ok)
     return fail(h, SW2D_EUNSUPPORTED, "cuStreamWaitValue32/WriteValue32 unavailable");
-  CUDA_TRY(h, cudaMalloc(&h->flags, 2 * sizeof(unsigned int)));
-  CUDA_TRY(h, cudaMemset(h->flags, 0, 2 * sizeof(unsigned int)));
-  constexpr int kH = 7;
-  Slab& sl = h->slabs[0];
-  void* mine[kH] = {sl.E[0], sl.E[1], sl.U[0], sl.U[1], sl.V[0], sl.V[1], h->flags};
-  std::vector<cudaIpcMemHandle_t> hs(kH);
-  for (int i = 0; i < kH; ++i) CUDA_TRY(h, cudaIpcGetMemHandle(&hs[i], mine[i]));
-  const size_t per = kH * sizeof(cudaIpcMemHandle_t);
+  std::vector<PeerBlob> bs((size_t)h->nranks);
+  for (int q = 0; q < h->nranks; ++q) {
+    std::memcpy(&bs[q], blobs + (size_t)q * SW2D_P2P_BLOB_BYTES, sizeof(PeerBlob));
+    const PeerBlob& b = bs[q];
+    int64_t j0 = 0, nrows = 0;
+    sw2d_partition(h->p.ny, h->nranks, q, &j0, &nrows);
+    if (b.magic != kBlobMagic || b.version != SW2D_ABI_VERSION || b.rank != q ||
+        b.nranks != h->nranks || b.nx != h->p.nx || b.ny != h->p.ny || b.pitch != h->pitch ||
+        b.j0 != j0 || b.nrows != nrows || b.xring != kXRing || b.nhandles != 8)
+      return fail(h, SW2D_EINVAL,
+                  "sw2d_p2p_import: blob " + std::to_string(q) +
+                      " does not match this grid / partition / rank order / library");
+  }
+  h->psync.assign((size_t)h->nranks, nullptr);
+  for (int q = 0; q < h->nranks; ++q) {
+    if (q == h->rank) continue;
+    void* p = nullptr;
+    CUDA_TRY(h, cudaIpcOpenMemHandle(&p, bs[q].mem[7], cudaIpcMemLazyEnablePeerAccess));
+    h->psync[q] = (unsigned char*)p;
+  }
+  for (int side = 0; side < 2; ++side) {
+    const int q = side == 0 ? h->rank - 1 : h->rank + 1;
+    if (q < 0 || q >= h->nranks) continue;
+    auto& pr = h->nbr[side];
+    void* p[7];
+    for (int i = 0; i < 7; ++i) {
+      CUDA_TRY(h, cudaIpcOpenMemHandle(&p[i], bs[q].mem[i], cudaIpcMemLazyEnablePeerAccess));
+      switch (i) {  // recorded one by one so free_all closes what was opened
+        case 0: pr.E[0] = (float*)p[i]; break;
+        case 1: pr.E[1] = (float*)p[i]; break;
+        case 2: pr.U[0] = (float*)p[i]; break;
+        case 3: pr.U[1] = (float*)p[i]; break;
+        case 4: pr.V[0] = (float*)p[i]; break;
+        case 5: pr.V[1] = (float*)p[i]; break;
+        default: pr.H0 = (float*)p[i]; break;
+      }
+    }
+    pr.jbase = bs[q].j0 + 1 - kHaloRows;
+    pr.nrows = bs[q].nrows;
+    pr.nelem = (bs[q].nrows + 2 * kHaloRows) * h->pitch;
+    pr.present = true;
+  }
+  h->p2p_ready = true;
+  return SW2D_OK;
+}
+
+// P2P with an NCCL bootstrap: the blobs travel by one NCCL all-gather at create.
+int setup_p2p_nccl(sw2d* h) {
+  const auto& nc = sw2d_host::nccl();
+  const size_t per = SW2D_P2P_BLOB_BYTES;
+  std::vector<unsigned char> mine(per), all(per * (size_t)h->nranks);
+  int rc = p2p_export(h, mine.data());
+  if (rc) return rc;
   unsigned char* dsend = nullptr;
   unsigned char* drecv = nullptr;
   CUDA_TRY(h, cudaMalloc(&dsend, per));
   CUDA_TRY(h, cudaMalloc(&drecv, per * (size_t)h->nranks));
-  std::vector<unsigned char> all(per * (size_t)h->nranks);
-  CUDA_TRY(h, cudaMemcpy(dsend, hs.data(), per, cudaMemcpyHostToDevice));
+  CUDA_TRY(h, cudaMemcpy(dsend, mine.data(), per, cudaMemcpyHostToDevice));
   NCCL_TRY(h, nc.AllGather(dsend, drecv, per, ncclUint8, h->comm_nccl, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   CUDA_TRY(h, cudaMemcpy(all.data(), drecv, all.size(), cudaMemcpyDeviceToHost));
   cudaFree(dsend);
   cudaFree(drecv);
+  return p2p_import(h, all.data());
+}
+
+// P2P mode, in sw2d_set_state: once each neighbour has finished every pass it
+// was given (its signals so far have arrived: it no longer reads its halos),
+// store this rank's boundary rows of hzero and of state 0 into its halo rows,
+// then signal it.  The first pass waits for that signal.
+int p2p_halo_init(sw2d* h) {
+  const auto& mo = sw2d_host::memops();
+  int64_t plan[4];
+  sw2d_halo_plan(h->p.ny, h->nranks, h->rank, plan);
+  Slab& sl = h->slabs[0];
+  const size_t bytes = (size_t)(kHaloRows * h->pitch) * sizeof(float);
   for (int side = 0; side < 2; ++side) {
-    const int peer = side == 0 ? h->rank - 1 : h->rank + 1;
-    if (peer < 0 || peer >= h->nranks) continue;
-    auto& pr = h->nbr[side];
-    const cudaIpcMemHandle_t* ph =
-        reinterpret_cast<const cudaIpcMemHandle_t*>(all.data() + per * (size_t)peer);
-    void* p[kH];
-    for (int i = 0; i < kH; ++i)
-      CUDA_TRY(h, cudaIpcOpenMemHandle(&p[i], ph[i], cudaIpcMemLazyEnablePeerAccess));
-    pr.E[0] = (float*)p[0]; pr.E[1] = (float*)p[1];
-    pr.U[0] = (float*)p[2]; pr.U[1] = (float*)p[3];
-    pr.V[0] = (float*)p[4]; pr.V[1] = (float*)p[5];
-    pr.flags = (unsigned int*)p[6];
-    int64_t j0, nrows;
-    sw2d_partition(h->p.ny, h->nranks, peer, &j0, &nrows);
-    pr.jbase = j0 + 1 - kHaloRows;
-    pr.nelem = (nrows + 2 * kHaloRows) * h->pitch;
-    pr.present = true;
+    const auto& pr = h->nbr[side];
+    if (!pr.present) continue;
+    if (mo.wait32(h->stream, flag_addr(h->sync, 0, side), h->hseq, 0x0))
+      return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
+    // rows this rank sends towards `side` land in the neighbour's halo facing us:
+    // its north halo (storage rows nrows+4..) for the south neighbour, its
+    // south halo (rows 0..3) for the north one
+    const int64_t send_row = plan[2 * side];
+    const int64_t recv_row = side == 0 ? pr.nrows + kHaloRows : 0;
+    const float* src[4] = {sl.H0, sl.E[0], sl.U[0], sl.V[0]};
+    float* dst[4] = {pr.H0, pr.E[0], pr.U[0], pr.V[0]};
+    for (int f = 0; f < 4; ++f)
+      CUDA_TRY(h, cudaMemcpyAsync(fld(dst[f], h->pitch, recv_row), fld((float*)src[f], h->pitch, send_row),
+                                  bytes, cudaMemcpyDeviceToDevice, h->stream));
   }
+  for (int side = 0; side < 2; ++side)
+    if (h->nbr[side].present &&
+        mo.write32(h->stream, flag_addr(h->psync[h->rank + (side ? 1 : -1)], 0, 1 - side),
+                   h->hseq + 1, 0x0))
+      return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
+  h->hseq++;
   return SW2D_OK;
 }
 
@@ -705,6 +955,13 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     if (dist->halo_mode != SW2D_HALO_NCCL && dist->halo_mode != SW2D_HALO_P2P)
       return fail(h, SW2D_EINVAL, "unknown halo_mode");
     h->halo_mode = dist->halo_mode;
+    if (dist->bootstrap != SW2D_BOOT_NCCL && dist->bootstrap != SW2D_BOOT_EXTERNAL)
+      return fail(h, SW2D_EINVAL, "unknown bootstrap");
+    h->bootstrap = dist->bootstrap;
+    if (h->multi && h->bootstrap == SW2D_BOOT_EXTERNAL && h->halo_mode != SW2D_HALO_P2P)
+      return fail(h, SW2D_EINVAL, "SW2D_BOOT_EXTERNAL needs SW2D_HALO_P2P");
+    if (h->multi && h->nranks > kMaxRanks)
+      return fail(h, SW2D_EUNSUPPORTED, "more than 128 real ranks");
     if (dist->device >= 0) CUDA_TRY(h, cudaSetDevice(dist->device));
   }
   CUDA_TRY(h, cudaGetDevice(&h->device));
@@ -791,22 +1048,32 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   CUDA_TRY(h, cudaMemsetAsync(h->counter, 0, 2 * sizeof(unsigned int), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->hist, sizeof(double) * kRecN * (size_t)h->hist_len));
   CUDA_TRY(h, cudaMemsetAsync(h->hist, 0, sizeof(double) * kRecN * (size_t)h->hist_len, h->stream));
-  CUDA_TRY(h, cudaMalloc(&h->rec, 2 * sizeof(double) * kRecN));  // scratch: up to 2 steps
+  // scratch: up to 2 steps' records, plus a discard record
+  CUDA_TRY(h, cudaMalloc(&h->rec, 3 * sizeof(double) * kRecN));
   CUDA_TRY(h, cudaMalloc(&h->h0sum, sizeof(double)));
   CUDA_TRY(h, cudaMalloc(&h->zero, sizeof(double)));
   CUDA_TRY(h, cudaMemsetAsync(h->zero, 0, sizeof(double), h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->h0sum, 0, sizeof(double), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->bad, sizeof(int)));
-  // NCCL communicator
+  // real ranks: the sync buffer (flags, record slots), then the NCCL
+  // communicator (SW2D_BOOT_NCCL), which in P2P mode only all-gathers the blobs
   if (h->multi) {
-    const auto& nc = sw2d_host::nccl();
-    if (!nc.ok) return fail(h, SW2D_ENCCL, std::string("NCCL unavailable: ") + nc.why);
-    ncclUniqueId id;
-    std::memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
-    NCCL_TRY(h, nc.CommInitRank(&h->comm_nccl, h->nranks, id, h->rank));
-    if (h->halo_mode == SW2D_HALO_P2P) {
-      int rc = setup_p2p(h);
-      if (rc) return rc;
+    h->sync_bytes = sync_size(h->nranks);
+    CUDA_TRY(h, cudaMalloc(&h->sync, h->sync_bytes));
+    CUDA_TRY(h, cudaMemsetAsync(h->sync, 0, h->sync_bytes, h->stream));
+    for (cudaEvent_t& e : h->ev_x) CUDA_TRY(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->psync.assign((size_t)h->nranks, nullptr);
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    if (h->bootstrap == SW2D_BOOT_NCCL) {
+      const auto& nc = sw2d_host::nccl();
+      if (!nc.ok) return fail(h, SW2D_ENCCL, std::string("NCCL unavailable: ") + nc.why);
+      ncclUniqueId id;
+      std::memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
+      NCCL_TRY(h, nc.CommInitRank(&h->comm_nccl, h->nranks, id, h->rank));
+      if (h->halo_mode == SW2D_HALO_P2P) {
+        int rc = setup_p2p_nccl(h);
+        if (rc) return rc;
+      }
     }
   }
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
@@ -839,11 +1106,27 @@ int run_pass(sw2d* h, int spl) {
   const auto& mo = sw2d_host::memops();
   const std::vector<Launch>& launches = spl == 2 ? h->launches2 : h->launches;
   const int blocks = spl == 2 ? h->step_blocks2 : h->step_blocks;
+  // dst: where each step's (global) record ends up; rec: where the kernels
+  // write it — the same, or with real ranks this rank's exchange slot
+  const bool xrec = h->multi && h->red_level;
   double* rec[2];
-  for (int k = 0; k < 2; ++k)
-    rec[k] = !h->red_level ? h->rec + k * kRecN
+  double* dst[2];
+  for (int k = 0; k < 2; ++k) {
+    dst[k] = !h->red_level ? h->rec + k * kRecN
              : h->capturing ? h->grec + (size_t)(h->cap_step + k) * kRecN
                             : h->hist + (size_t)((h->steps + k) % h->hist_len) * kRecN;
+    rec[k] = xrec ? xslot(h->sync, h->nranks, h->xseq + (uint64_t)k, h->rank) : dst[k];
+  }
+  // a one-record ring keeps only the pass's second record (two writers of one
+  // slot would race): the first goes to a discard record
+  if (spl == 2 && h->red_level && !h->capturing && h->hist_len == 1) {
+    dst[0] = h->rec + 2 * kRecN;
+    if (!xrec) rec[0] = dst[0];
+  }
+  if (xrec) {
+    int rc = guard_slots(h, h->xseq, spl);
+    if (rc) return rc;
+  }
   // captured two-step small-grid passes defer their diagnostics: CTA partials
   // go to gpart[step within the graph], folded by fold_steps at the graph's end
   const bool defer = h->capturing && h->red_level && spl == 2 && h->kind == 2;
@@ -862,11 +1145,8 @@ int run_pass(sw2d* h, int spl) {
     int rc = nccl_halo(h, h->cur, h->comm);
     if (rc) return rc;
     CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
-    for (int64_t st : h->pending) {  // the previous pass's diagnostics
-      rc = nccl_allreduce_rec(h, h->hist + (size_t)(st % h->hist_len) * kRecN, h->comm);
-      if (rc) return rc;
-    }
-    h->pending.clear();
+    rc = flush_pending(h);  // the previous pass's diagnostics, behind the exchange
+    if (rc) return rc;
   }
   auto args = [&](const Launch& L) {
     StepArgs a = step_args(h, L, rec[0]);
@@ -897,10 +1177,12 @@ int run_pass(sw2d* h, int spl) {
   for (const Launch& L : launches) any1 |= L.phase == 1;
   if (any1 && h->multi) {
     if (p2p) {
-      const unsigned want = (unsigned)h->steps;  // neighbours have finished step want-1
+      // every signal sent to us so far has arrived: the neighbour's previous
+      // pass (or its set_state) has stored our halo rows and no longer reads
+      // its own halo rows of the buffer this pass writes
       for (int side = 0; side < 2; ++side)
         if (h->nbr[side].present &&
-            mo.wait32(h->stream, (unsigned long long)(h->flags + side), want, 0x0 /*GEQ*/))
+            mo.wait32(h->stream, flag_addr(h->sync, 0, side), h->hseq, 0x0 /*GEQ*/))
           return fail(h, SW2D_ECUDA, "cuStreamWaitValue32 failed");
     } else {
       CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
@@ -915,24 +1197,23 @@ int run_pass(sw2d* h, int spl) {
   CUDA_TRY(h, cudaGetLastError());
   if (h->multi) {
     if (p2p) {  // tell the neighbours this pass's rows have landed in their halos
-      const unsigned done = (unsigned)(h->steps + spl);
       for (int side = 0; side < 2; ++side)
         if (h->nbr[side].present &&
-            mo.write32(h->stream, (unsigned long long)(h->nbr[side].flags + (1 - side)), done,
-                       0x0))
+            mo.write32(h->stream, flag_addr(h->psync[h->rank + (side ? 1 : -1)], 0, 1 - side),
+                       h->hseq + 1, 0x0))
           return fail(h, SW2D_ECUDA, "cuStreamWriteValue32 failed");
+      h->hseq++;
     }
     CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
-    if (h->red_level) {
+    if (xrec) {
       if (p2p) {
         CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-        for (int k = 0; k < spl; ++k) {
-          int rc = nccl_allreduce_rec(h, rec[k], h->comm);
-          if (rc) return rc;
-        }
+        int rc = p2p_exchange(h, h->xseq, spl, dst[0], dst[1]);
+        if (rc) return rc;
       } else {
-        for (int k = 0; k < spl; ++k) h->pending.push_back(h->steps + k);
+        for (int k = 0; k < spl; ++k) h->pending.push_back({h->xseq + (uint64_t)k, dst[k]});
       }
+      h->xseq += (uint64_t)spl;
     }
   }
   h->cur = 1 - h->cur;
@@ -1008,10 +1289,34 @@ int sw2d_create(const sw2d_params* params, const sw2d_dist* dist,
   return SW2D_OK;
 }
 
+int sw2d_p2p_export(sw2d* h, void* out, size_t cap) {
+  NvtxRange nvtx_("sw2d_p2p_export");
+  ENTER(h);
+  if (!out || cap < SW2D_P2P_BLOB_BYTES)
+    return fail(h, SW2D_EINVAL, "sw2d_p2p_export: out needs SW2D_P2P_BLOB_BYTES");
+  return p2p_export(h, (unsigned char*)out);
+}
+
+int sw2d_p2p_import(sw2d* h, const void* blobs, size_t nbytes) {
+  NvtxRange nvtx_("sw2d_p2p_import");
+  ENTER(h);
+  if (!blobs || nbytes != (size_t)SW2D_P2P_BLOB_BYTES * (size_t)h->nranks)
+    return fail(h, SW2D_EINVAL, "sw2d_p2p_import: need nranks * SW2D_P2P_BLOB_BYTES bytes");
+  return p2p_import(h, (const unsigned char*)blobs);
+}
+
 int sw2d_local_rows(const sw2d* h, int64_t* j0, int64_t* nrows) {
   if (!h || !j0 || !nrows) return SW2D_EINVAL;
   *j0 = h->slabs.front().j0;
   *nrows = h->slabs.back().j0 + h->slabs.back().nrows - h->slabs.front().j0;
+  return SW2D_OK;
+}
+
+int sw2d_local_shape(const sw2d* h, int64_t* nrows, int64_t* nx) {
+  int64_t j0 = 0;
+  const int rc = sw2d_local_rows(h, &j0, nrows);
+  if (rc != SW2D_OK || !nx) return SW2D_EINVAL;
+  *nx = h->p.nx;
   return SW2D_OK;
 }
 
@@ -1020,6 +1325,8 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
   NvtxRange nvtx_("sw2d_set_state");
   ENTER(h);
   if (!hzero || !eta) return fail(h, SW2D_EINVAL, "hzero and eta are required");
+  if (p2p_real(h) && !h->p2p_ready)
+    return fail(h, SW2D_ESTATE, "P2P ranks: sw2d_p2p_import before sw2d_set_state");
   const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
   const size_t wbytes = (size_t)nx * sizeof(float);
   const size_t dp = (size_t)h->pitch * sizeof(float);
@@ -1071,18 +1378,19 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
   CUDA_TRY(h, cudaMemcpyAsync(h->h0sum, h->rec + kRecSumEta, sizeof(double),
                               cudaMemcpyDeviceToDevice, h->stream));
   // static hzero halo, once; in P2P mode also the state-0 halos (later steps
-  // deliver them with the boundary rows).  The flags are reset before the
-  // exchange: a neighbour can signal only after it has exchanged with us.
+  // deliver them with the boundary rows): NCCL exchange, device copies between
+  // virtual slabs, or stores into the neighbours' halos plus a signal (P2P).
   const bool p2p = h->halo_mode == SW2D_HALO_P2P;
-  if (h->flags) CUDA_TRY(h, cudaMemsetAsync(h->flags, 0, 2 * sizeof(unsigned int), h->stream));
   if (h->virt) {
     int rc = virtual_halo(h, -1);
     if (rc) return rc;
     if (p2p && (rc = virtual_halo(h, 0))) return rc;
+  } else if (h->multi && p2p) {
+    int rc = p2p_halo_init(h);
+    if (rc) return rc;
   } else if (h->multi) {
     int rc = nccl_halo(h, -1, h->stream);
     if (rc) return rc;
-    if (p2p && (rc = nccl_halo(h, 0, h->stream))) return rc;
   }
   h->wcur = 0;
   if (h->p.variant == SW2D_VARIANT_PAPER) {
@@ -1222,11 +1530,8 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
   }
   if (h->multi && !h->pending.empty()) {
     CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
-    for (int64_t st : h->pending) {
-      int rc = nccl_allreduce_rec(h, h->hist + (size_t)(st % h->hist_len) * kRecN, h->comm);
-      if (rc) return rc;
-    }
-    h->pending.clear();
+    int rc = flush_pending(h);
+    if (rc) return rc;
   }
   if (h->multi && h->red_level) {
     // later work on the compute stream (reads of the history) follows the allreduces
@@ -1294,7 +1599,7 @@ int sw2d_sync(sw2d* h) {
   ENTER(h);
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
   if (h->comm) CUDA_TRY(h, cudaStreamSynchronize(h->comm));
-  if (h->multi) {
+  if (h->comm_nccl) {
     ncclResult_t ar = ncclSuccess;
     NCCL_TRY(h, sw2d_host::nccl().CommGetAsyncError(h->comm_nccl, &ar));
     NCCL_TRY(h, ar);
@@ -1307,13 +1612,21 @@ int sw2d_reduce(sw2d* h, int op, double* out) {
   ENTER(h);
   if (!out || op < 0 || op >= SW2D_RED_N) return fail(h, SW2D_EINVAL, "bad op / out");
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_reduce before sw2d_set_state");
-  {
+  if (p2p_real(h)) {  // this rank's record in its exchange slot, combined on comm
+    int rc = guard_slots(h, h->xseq, 1);
+    if (!rc) rc = reduce_into(h, xslot(h->sync, h->nranks, h->xseq, h->rank));
+    if (rc) return rc;
+    CUDA_TRY(h, cudaEventRecord(h->ev_ready, h->stream));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->comm, h->ev_ready, 0));
+    rc = p2p_exchange(h, h->xseq, 1, h->rec, nullptr);
+    if (rc) return rc;
+    h->xseq++;
+    CUDA_TRY(h, cudaEventRecord(h->ev_halo, h->comm));
+    CUDA_TRY(h, cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+  } else {
     int rc = reduce_into(h, h->rec);
     if (rc) return rc;
-  }
-  if (h->multi) {
-    int rc = nccl_allreduce_rec(h, h->rec, h->stream);
-    if (rc) return rc;
+    if (h->multi && (rc = nccl_allreduce_rec(h, h->rec, h->rec, h->stream))) return rc;
   }
   double rec[kRecN];
   CUDA_TRY(h, cudaMemcpyAsync(rec, h->rec, sizeof(rec), cudaMemcpyDeviceToHost, h->stream));

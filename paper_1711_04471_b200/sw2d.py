@@ -27,10 +27,13 @@ SW2D_RED_N = 7
 SW2D_VARIANT_FUSED = 0
 SW2D_VARIANT_PAPER = 1
 SW2D_HALO_NCCL, SW2D_HALO_P2P = 0, 1
+SW2D_BOOT_NCCL, SW2D_BOOT_EXTERNAL = 0, 1
+SW2D_P2P_BLOB_BYTES = 1024
 
 #: every symbol include/sw2d.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("sw2d_abi_version", "sw2d_partition", "sw2d_halo_plan", "sw2d_nccl_unique_id",
-           "sw2d_create", "sw2d_local_rows", "sw2d_set_state", "sw2d_step",
+           "sw2d_create", "sw2d_p2p_export", "sw2d_p2p_import",
+           "sw2d_local_rows", "sw2d_local_shape", "sw2d_set_state", "sw2d_step",
            "sw2d_run_snapshots", "sw2d_reduce", "sw2d_reduce_history", "sw2d_get_state",
            "sw2d_sync", "sw2d_plan",
            "sw2d_launch_count", "sw2d_destroy", "sw2d_strerror",
@@ -55,7 +58,8 @@ class sw2d_params(ctypes.Structure):
 class sw2d_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("virtual_ranks", ctypes.c_int32),
-                ("halo_mode", ctypes.c_int32), ("nccl_id", ctypes.c_ubyte * 128)]
+                ("halo_mode", ctypes.c_int32), ("nccl_id", ctypes.c_ubyte * 128),
+                ("bootstrap", ctypes.c_int32)]
 
 
 _lib = None
@@ -79,7 +83,10 @@ def load(path: str = _LIB_PATH):
         "sw2d_nccl_unique_id": ([vp], ctypes.c_int),
         "sw2d_create": ([ctypes.POINTER(sw2d_params), ctypes.POINTER(sw2d_dist), vp,
                          ctypes.POINTER(vp)], ctypes.c_int),
+        "sw2d_p2p_export": ([vp, vp, ctypes.c_size_t], ctypes.c_int),
+        "sw2d_p2p_import": ([vp, vp, ctypes.c_size_t], ctypes.c_int),
         "sw2d_local_rows": ([vp, p64, p64], ctypes.c_int),
+        "sw2d_local_shape": ([vp, p64, p64], ctypes.c_int),
         "sw2d_set_state": ([vp, vp, vp, vp, vp], ctypes.c_int),
         "sw2d_step": ([vp, i64], ctypes.c_int),
         "sw2d_run_snapshots": ([vp, i64, i64, vp, i64], ctypes.c_int),
@@ -108,21 +115,35 @@ def _check(rc: int, h=None):
         raise Sw2dError(rc, detail)
 
 
-def _ptr(a, dtype=np.float32, writable=False):
-    """Pointer of a C-contiguous numpy array / torch tensor (host or CUDA)."""
+def _ptr(a, dtype=np.float32, writable=False, need=None):
+    """Pointer of a C-contiguous numpy array / torch tensor (host or CUDA)
+    holding at least `need` elements (the C side reads / writes that many)."""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):  # torch.Tensor
         import torch
-        want = torch.float32 if dtype == np.float32 else torch.uint8
+        want = {np.float32: torch.float32, np.float64: torch.float64,
+                np.uint8: torch.uint8}[dtype]
         if a.dtype != want or not a.is_contiguous():
             raise TypeError(f"tensor must be contiguous {want}")
-        return ctypes.c_void_p(a.data_ptr())
-    if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
-        raise TypeError(f"array must be a C-contiguous numpy {np.dtype(dtype).name} array")
-    if writable and not a.flags.writeable:
-        raise TypeError("output array is read-only")
-    return ctypes.c_void_p(a.ctypes.data)
+        size = a.numel()
+        ptr = a.data_ptr()
+    else:
+        if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
+            raise TypeError(f"array must be a C-contiguous numpy {np.dtype(dtype).name} array")
+        if writable and not a.flags.writeable:
+            raise TypeError("output array is read-only")
+        size = a.size
+        ptr = a.ctypes.data
+    if need is not None and size < need:
+        raise ValueError(f"array holds {size} elements, the call needs {need}")
+    return ctypes.c_void_p(ptr)
+
+
+def _cells(h) -> int:
+    """Elements of one [nrows][nx] field of the rows the handle holds."""
+    n, nx = sw2d_local_shape(h)
+    return n * nx
 
 
 def make_params(nx, ny, dx=1.0, dy=1.0, dt=0.01, g=9.81, eps=0.05, hmin=0.05,
@@ -134,10 +155,11 @@ def make_params(nx, ny, dx=1.0, dy=1.0, dt=0.01, g=9.81, eps=0.05, hmin=0.05,
 
 
 def make_dist(rank=0, nranks=1, device=-1, virtual_ranks=0, nccl_id=None,
-              halo_mode=0) -> sw2d_dist:
+              halo_mode=0, bootstrap=SW2D_BOOT_NCCL) -> sw2d_dist:
     d = sw2d_dist(int(rank), int(nranks), int(device), int(virtual_ranks), int(halo_mode))
     if nccl_id is not None:
         ctypes.memmove(d.nccl_id, bytes(nccl_id), 128)
+    d.bootstrap = int(bootstrap)
     return d
 
 
@@ -187,14 +209,38 @@ def sw2d_create(params: sw2d_params, dist: sw2d_dist | None = None, stream=None)
     return h
 
 
+def sw2d_p2p_export(h) -> bytes:
+    """This rank's peer blob (SW2D_P2P_BLOB_BYTES bytes) for sw2d_p2p_import."""
+    buf = (ctypes.c_ubyte * SW2D_P2P_BLOB_BYTES)()
+    _check(load().sw2d_p2p_export(h, buf, SW2D_P2P_BLOB_BYTES), h)
+    return bytes(buf)
+
+
+def sw2d_p2p_import(h, blobs) -> None:
+    """``blobs``: every rank's blob in rank order (a list of bytes, or their
+    concatenation)."""
+    data = b"".join(blobs) if isinstance(blobs, (list, tuple)) else bytes(blobs)
+    buf = (ctypes.c_ubyte * len(data)).from_buffer_copy(data)
+    _check(load().sw2d_p2p_import(h, buf, len(data)), h)
+
+
 def sw2d_local_rows(h):
     j0, n = ctypes.c_int64(), ctypes.c_int64()
     _check(load().sw2d_local_rows(h, ctypes.byref(j0), ctypes.byref(n)), h)
     return j0.value, n.value
 
 
+def sw2d_local_shape(h):
+    """(nrows, nx) of the [nrows][nx] host-visible arrays of this handle."""
+    n, nx = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().sw2d_local_shape(h, ctypes.byref(n), ctypes.byref(nx)), h)
+    return n.value, nx.value
+
+
 def sw2d_set_state(h, hzero, eta, u=None, v=None) -> None:
-    _check(load().sw2d_set_state(h, _ptr(hzero), _ptr(eta), _ptr(u), _ptr(v)), h)
+    c = _cells(h)
+    _check(load().sw2d_set_state(h, _ptr(hzero, need=c), _ptr(eta, need=c), _ptr(u, need=c),
+                                 _ptr(v, need=c)), h)
 
 
 def sw2d_step(h, nsteps: int) -> None:
@@ -205,8 +251,8 @@ def sw2d_run_snapshots(h, nsteps: int, every: int, out_eta) -> None:
     """Run nsteps; out_eta [nsnap][nrows][nx] float32 receives eta after every
     `every` steps (nsnap = nsteps // every)."""
     nsnap = int(nsteps) // int(every) if every else -1
-    _check(load().sw2d_run_snapshots(h, int(nsteps), int(every), _ptr(out_eta, writable=True),
-                                     nsnap), h)
+    out = _ptr(out_eta, writable=True, need=max(nsnap, 0) * _cells(h))
+    _check(load().sw2d_run_snapshots(h, int(nsteps), int(every), out, nsnap), h)
 
 
 def sw2d_reduce(h, op: int) -> float:
@@ -217,13 +263,16 @@ def sw2d_reduce(h, op: int) -> float:
 
 def sw2d_reduce_history(h, op: int, n: int, out=None) -> np.ndarray:
     out = np.empty(int(n), np.float64) if out is None else out
-    _check(load().sw2d_reduce_history(h, int(op), _ptr(out, np.float64, True), int(n)), h)
+    _check(load().sw2d_reduce_history(h, int(op), _ptr(out, np.float64, True, need=int(n)),
+                                      int(n)), h)
     return out
 
 
 def sw2d_get_state(h, eta=None, u=None, v=None, wet=None) -> None:
-    _check(load().sw2d_get_state(h, _ptr(eta, writable=True), _ptr(u, writable=True),
-                                 _ptr(v, writable=True), _ptr(wet, np.uint8, True)), h)
+    c = _cells(h)
+    _check(load().sw2d_get_state(h, _ptr(eta, writable=True, need=c),
+                                 _ptr(u, writable=True, need=c), _ptr(v, writable=True, need=c),
+                                 _ptr(wet, np.uint8, True, need=c)), h)
 
 
 def sw2d_sync(h) -> None:

@@ -668,28 +668,42 @@ def test_even_split_virtual_ranks_bitwise(halo, monkeypatch):
 
 
 @pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
-def test_single_rank_nccl_machinery(halo, monkeypatch):
+@pytest.mark.parametrize("history_len", [1, 3, 0])
+def test_single_rank_nccl_machinery(halo, history_len, monkeypatch):
     """One real rank with the NCCL path forced on (SW2D_FORCE_NCCL): the
     library's NCCL communicator, comm stream, grouped halo exchange (no
-    peers), per-step diagnostics allreduces and, in P2P mode, the IPC-handle
-    all-gather all run on the GPU; fields stay bitwise and every per-step
-    record equals the oracle's.  (Two real ranks need two GPUs.)"""
+    peers), the per-step records' out-of-place allreduce (NCCL mode) or slot
+    exchange (P2P mode, here with itself) and, in P2P mode, the blob
+    all-gather all run on the GPU; fields stay bitwise and every kept
+    per-step record equals the oracle's — also with history rings shorter
+    than the run (1 and 3 records for 23 steps: ADVICE r01 #1) and over 150
+    steps (the 64-record exchange ring wraps).  Real ranks sharing the GPU:
+    tests/test_gpu_p2p_procs.py."""
     monkeypatch.setenv("SW2D_FORCE_NCCL", "1")
     cfg, st = _bowl(300, 200)
-    n = 23
-    want = oracle_run(P, st, n, history=True)
+    hz, e, u, v = st
     uid = sw2d.sw2d_nccl_unique_id()
-    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL,
-                                dist=sw2d.make_dist(0, 1, 0, 0, uid, halo))
-    assert_state_equal(got, want[:4], where=f"forced NCCL, halo {halo}")
-    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
-    for op, series in hist.items():
-        for k in range(n):
-            row = np.zeros(oracle.NRED)
-            row[op] = series[k]
-            ref = np.zeros(oracle.NRED)
-            ref[op] = want[4][k, op]
-            check_reductions(row, ref)
+    p = sw2d.make_params(300, 200, P["dx"], P["dy"], P["dt"], P["g"], P["eps"], P["hmin"],
+                         reduce_every_step=ALL, history_len=history_len)
+    h = sw2d.sw2d_create(p, sw2d.make_dist(0, 1, 0, 0, uid, halo))
+    try:
+        for chunks in ([23], [7, 1, 80, 62]):
+            n = sum(chunks)
+            want = oracle_run(P, st, n, history=True)
+            sw2d.sw2d_set_state(h, hz, e, u, v)
+            for c in chunks:
+                sw2d.sw2d_step(h, c)
+            got = sw2d.get_state(h, 300)
+            keep = min(n, history_len or 1024)
+            hist = {op: sw2d.sw2d_reduce_history(h, op, keep) for op in range(sw2d.SW2D_RED_N)}
+            red = [sw2d.sw2d_reduce(h, op) for op in range(sw2d.SW2D_RED_N)]
+            assert_state_equal(got, want[:4], where=f"forced NCCL, halo {halo}, {chunks}")
+            check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+            for k in range(keep):
+                check_reductions([hist[op][k] for op in range(sw2d.SW2D_RED_N)],
+                                 want[4][n - keep + k])
+    finally:
+        sw2d.sw2d_destroy(h)
 
 
 def test_legacy_default_stream_long_run():
