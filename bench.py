@@ -312,6 +312,8 @@ def run_ours(args, cfg, ws, rank, local):
         obj = [sw2d.sw2d_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    elif os.environ.get("SW2D_FORCE_NCCL", "0") != "0":
+        uid = sw2d.sw2d_nccl_unique_id()   # one real rank with the NCCL machinery (A/B)
     stream = torch.cuda.Stream()          # the handle's stream; events are recorded on it
     torch.cuda.set_stream(stream)
     p = sw2d.make_params(nx, ny, cfg["dx"], cfg["dy"], cfg["dt"], cfg["g"], cfg["eps"],
@@ -360,18 +362,18 @@ def run_ours(args, cfg, ws, rank, local):
         # boundary launches per step are timed together).
         red_lvl = 0 if not mask else (1 if mask < 4 else 2)
         launches_per_step = launches / (T * args.steps)
-        spl = 2 if (args.variant == "fused" and launches_per_step < 0.75) else 1
+        plan = dict(kv.split("=") for kv in sw2d.sw2d_plan(h).split())
+        spl = int(plan.get("steps_per_launch", "1")) if args.variant == "fused" else 1
         t_launch_s = ms * 1e-3 / (T * args.steps) * spl
         cells_local = nrows * nx
         bpc = BYTES_PER_CELL if args.variant == "fused" else PAPER_BYTES_PER_CELL
         alg_bytes = bpc * cells_local            # state in + state out, per launch
         hbm_achieved = alg_bytes / t_launch_s / 1e9
         peak, peak_src = hbm_peak()
-        plan = dict(kv.split("=") for kv in sw2d.sw2d_plan(h).split())
-        if spl == 2:
+        if plan.get("kernel") == "small":
+            kname = ("sw2d_step_small2<%d>" if spl == 2 else "sw2d_step_small<%d>") % red_lvl
+        elif spl == 2:
             kname = "sw2d_step_cta2<%d>" % red_lvl
-        elif plan.get("kernel") == "small":
-            kname = "sw2d_step_small<%d>" % red_lvl
         else:
             kname = "sw2d_step_cta<%d, 0>" % red_lvl
         if args.variant != "fused":

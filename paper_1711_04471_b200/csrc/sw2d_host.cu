@@ -322,7 +322,6 @@ void plan_tb(sw2d* h, int sms) {
   h->tb_k = K;
 }
 
-constexpr int kSkReserveSms = 4;   // SMs left free by the even split with real ranks
 
 void plan_launches(sw2d* h) {
   int sms = 148;
@@ -364,12 +363,14 @@ void plan_launches(sw2d* h) {
       // group-rows evenly over one CTA per SM instead, if that lowers the
       // busiest CTA's streamed rows (each piece streams 8 extra rows; a share
       // may span two groups).  sms >= 2 x groups keeps a share within two.
-      // With real ranks a few SMs stay free: a step CTA holds a whole SM
-      // (registers), so the halo exchange's NCCL kernels and the boundary-band
-      // launches that overlap the interior launch need SMs of their own.
+      // Real ranks use every SM too: the boundary bands follow the interior
+      // launch on the same stream (they need the halo), the P2P transport
+      // runs no kernel beside it, and the NCCL exchange kernels (comm stream,
+      // highest priority) are dispatched ahead of the interior launch's CTAs
+      // when both become ready at the end of the previous pass.
       if (kind == 3 && sk_on) {
         const long long ncc = (nstrips + per - 1) / per;
-        const long long skc = h->multi ? std::max(1, sms - kSkReserveSms) : sms;
+        const long long skc = sms;
         const long long classic = std::min<long long>(rps, rows) + 8;   // rows per CTA
         const long long even = (rows * ncc + skc - 1) / skc + 2 * 8;
         if (sk_force > 0 && sk_force >= 2 * ncc) {   // tests: SW2D_SK=2 [SW2D_SK_CTAS=n]
@@ -1007,7 +1008,11 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   }
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_ready, cudaEventDisableTiming));
   CUDA_TRY(h, cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming));
-  if (h->multi) CUDA_TRY(h, cudaStreamCreateWithFlags(&h->comm, cudaStreamNonBlocking));
+  if (h->multi) {  // the comm stream's small kernels go ahead of pending step CTAs
+    int lo = 0, hi = 0;
+    CUDA_TRY(h, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(h, cudaStreamCreateWithPriority(&h->comm, cudaStreamNonBlocking, hi));
+  }
   // fields: (nrows + 4) x pitch floats each, zeroed (halo rows / columns stay 0)
   for (Slab& s : h->slabs) {
     const size_t bytes = (size_t)(s.nrows + 2 * kHaloRows) * (size_t)h->pitch * sizeof(float);

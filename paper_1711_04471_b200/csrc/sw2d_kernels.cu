@@ -389,6 +389,45 @@ __device__ __forceinline__ void vmul2(float& d0, float& d1, float a0, float a1, 
   d1 = __fmul_rn(a1, b1);
 }
 #undef SW2D_PAIR_ASM
+
+// sel(w, x) + y with a wet flag w in {0, 1}: the product w * x is exact (x or
+// a zero), so the fused multiply-add rounds once exactly where the oracle's
+// select-then-add rounds once: bitwise the same value (R24).  Only
+// these flag products are ever fused; SW2D_EXACT_FMA=0 builds mul + add.
+#ifndef SW2D_EXACT_FMA
+#define SW2D_EXACT_FMA 1
+#endif
+__device__ __forceinline__ float selfma(float w, float x, float y) {
+#if SW2D_EXACT_FMA
+  return __fmaf_rn(w, x, y);
+#else
+  return __fadd_rn(__fmul_rn(w, x), y);
+#endif
+}
+// packed pair form (fma.rn.f32x2 -> FFMA2), same exactness argument per element
+__device__ __forceinline__ void selfma2(float& d0, float& d1, float w0, float w1, float x0,
+                                        float x1, float y0, float y1) {
+#if SW2D_EXACT_FMA && SW2D_F32X2
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(w0), "f"(w1), "f"(x0), "f"(x1), "f"(y0), "f"(y1));
+#else
+  d0 = selfma(w0, x0, y0);
+  d1 = selfma(w1, x1, y1);
+#endif
+}
+template <int C, bool P = true>
+__device__ __forceinline__ void vselfma(float (&d)[C], const float (&w)[C], const float (&x)[C],
+                                        const float (&y)[C]) {
+#pragma unroll
+  for (int c = 0; c < C; c += (P ? 2 : 1)) {
+    if (P && c + 1 < C)
+      selfma2(d[c], d[c + 1], w[c], w[c + 1], x[c], x[c + 1], y[c], y[c + 1]);
+    else
+      d[c] = selfma(w[c], x[c], y[c]);
+  }
+}
 #define SW2D_PAIR_OP(NAME, SCALAR)                                                          \
   template <int C, bool P = true>                                                            \
   __device__ __forceinline__ void NAME(float (&d)[C], const float (&a)[C],                   \
@@ -514,8 +553,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
 
   // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
   float En[C], t3[C];
-  vmul<C, kPack>(t3, w.w1, et);
-  vadd<C, kPack>(t3, t3, w.sS);
+  vselfma<C, kPack>(t3, w.w1, et, w.sS);   // sel(wN, etan(L-1)) + sS
   vmul<C, kPack>(t3, x.q, t3);
   vadd<C, kPack>(t3, w.A, t3);
 #pragma unroll
@@ -538,9 +576,8 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   vmul<C, kPack>(sc, x.q, sc);
   vsub<C, kPack>(sc, 1.0f, sc);
   vmul<C, kPack>(t1, sc, et);
-  vmul<C, kPack>(xE, wE, eE);
   vmul<C, kPack>(xW, wW, eW);
-  vadd<C, kPack>(xE, xE, xW);
+  vselfma<C, kPackS>(xE, wE, eE, xW);      // sel(wE, etanE) + sel(wW, etanW)
   vmul<C, kPack>(xE, x.q, xE);
   vadd<C, kPack>(o.A, t1, xE);
   vmul<C, kPack>(o.sS, w.w2, w.etC);
@@ -1691,6 +1728,7 @@ int grid_stride_blocks(long long n) {
 
 }  // namespace
 
+#ifndef SW2D_PROBE   // tools/cta2_probe.cu: the kernels alone, one instantiation (SASS studies)
 int step_strips_per_cta(int kind) {
   return kind == 1 ? kCtaStrips : (kind == 2 ? kSmallWarps : kStepWarps);
 }
@@ -1873,5 +1911,7 @@ void launch_wet(const float* E, const float* H0, long long pitch,
   sw2d_wet_mask<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(E, H0, pitch, nrows,
                                                                nx, hmin, out);
 }
+
+#endif  // SW2D_PROBE
 
 }  // namespace sw2d_dev
