@@ -56,11 +56,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=(), debug: bool = False) -> str:
-    out = DEBUG_LIB if debug else LIB
+def build(force: bool = False, verbose: bool = False, extra=(), debug: bool = False,
+          out: str | None = None) -> str:
+    """Build libsw2d.so (or `out`: an A/B variant built with `extra` flags)."""
+    variant = out is not None
+    out = out or (DEBUG_LIB if debug else LIB)
     if debug:
         extra = (*extra, "-DSW2D_DEBUG_BOUNDS")
-    elif not force and not _stale():
+    elif not force and not variant and not _stale():
         return LIB
     tmp = out + f".tmp{os.getpid()}"
     objdir = out + f".obj{os.getpid()}"
@@ -91,6 +94,13 @@ def build(force: bool = False, verbose: bool = False, extra=(), debug: bool = Fa
 
 
 if __name__ == "__main__":
+    # python -m paper_1711_04471_b200._build [-v] [--ptxas] [--debug]
+    #        [--out path -DFLAG=1 ...]   (A/B variants: extra nvcc flags after --out)
     v = "-v" in sys.argv
     extra = ["-Xptxas", "-v"] if "--ptxas" in sys.argv else []
-    print(build(force=True, verbose=v, extra=extra, debug="--debug" in sys.argv))
+    out = None
+    if "--out" in sys.argv:
+        i = sys.argv.index("--out")
+        out = sys.argv[i + 1]
+        extra += [a for a in sys.argv[i + 2:] if a.startswith("-D")]
+    print(build(force=True, verbose=v, extra=extra, debug="--debug" in sys.argv, out=out))

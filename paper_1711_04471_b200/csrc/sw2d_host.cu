@@ -72,6 +72,12 @@ struct sw2d {
   int64_t fault_skip_halo = -1;  // SW2D_FAULT_SKIP_HALO (tests only)
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
   int tb_tw = 0, tb_th = 0, tb_k = 0;  // temporal blocking (small grids); tb_k = 0: off
+  // persistent cooperative kernel (small grids): K steps per shared-memory
+  // block, pntx x pnty tiles of pth rows, one CTA each; pk = 0: off
+  int pk = 0, pth = 0, pntx = 0, pnty = 0;
+  unsigned* pflags = nullptr;   // per-tile step counters
+  unsigned pbase = 0;           // their value before the next launch
+  RedPartial* ppart = nullptr;  // per-step CTA partials of one launch chunk
   std::vector<Slab> slabs;
   std::vector<Launch> launches;
   int step_blocks = 0;
@@ -286,6 +292,7 @@ Coef make_coef(const sw2d_params& p) {
   c.cy = (float)((double)p.dt / (double)p.dy);
   c.q = 0.25f * p.eps;
   c.hmin = p.hmin;
+  c.nz = -0.0f;
   return c;
 }
 
@@ -322,6 +329,44 @@ void plan_tb(sw2d* h, int sms) {
   h->tb_k = K;
 }
 
+
+// Small grids (the paper's 500^2, 1000^2): the persistent cooperative kernel
+// (sw2d_persist.cu), on one GPU without ranks, if its tiles fit co-resident.
+// Tile rows: the smallest of the candidates whose tiles all fit (more tiles,
+// more parallelism), SW2D_PERSIST_TH overrides; K = 2 steps per block
+// (SW2D_PERSIST_K).  SW2D_PERSIST=0: the graph-replayed small kernels.
+constexpr int kPersistRedChunk = 64;   // steps per launch when diagnostics are folded
+void plan_persist(sw2d* h) {
+  h->pk = 0;
+  const long long cells = h->p.nx * h->p.ny;
+  if (h->multi || h->virt || h->p.variant != SW2D_VARIANT_FUSED || h->slabs.size() != 1) return;
+  if (cells > kSmallMaxCells) return;
+  const char* on = std::getenv("SW2D_PERSIST");
+  if (!on || std::atoi(on) == 0) return;   // opt-in until it beats the graphs
+  // a forced kernel kind or the temporal-blocking experiment (tests, A/B) wins
+  if (!on && (std::getenv("SW2D_STEP_KERNEL") || h->tb_k)) return;
+  int K = 2;
+  if (const char* e = std::getenv("SW2D_PERSIST_K")) K = std::atoi(e) == 1 ? 1 : 2;
+  const int tw = persist_tile_cols(K);
+  const int ntx = (int)((h->p.nx + tw - 1) / tw);
+  static const int cand[] = {4, 8, 12, 16, 24, 32, 48, 64, 96, 128};
+  int th_force = 0;
+  if (const char* e = std::getenv("SW2D_PERSIST_TH")) th_force = std::max(1, std::atoi(e));
+  for (int th : cand) {
+    if (th_force) th = th_force;
+    if (persist_smem_bytes(K, th) > 226 * 1024) break;
+    const int nty = (int)((h->p.ny + th - 1) / th);
+    const int cap = persist_capacity(K, h->red_level, th);
+    if ((long long)ntx * nty <= cap) {
+      h->pk = K;
+      h->pth = th;
+      h->pntx = ntx;
+      h->pnty = nty;
+      return;
+    }
+    if (th_force) return;
+  }
+}
 
 void plan_launches(sw2d* h) {
   int sms = 148;
@@ -423,6 +468,7 @@ void plan_launches(sw2d* h) {
                            h->nstrips2);
   }
   plan_tb(h, sms);
+  plan_persist(h);
   {
     static const char* kinds[] = {"warp-ring", "cta-ring", "small"};
     std::string split = "grid";   // even-rows:<CTAs> if any two-step launch splits rows
@@ -437,6 +483,14 @@ void plan_launches(sw2d* h) {
                   bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k,
                   split.c_str());
     h->plan_text = buf;
+    if (h->pk) {
+      std::snprintf(buf, sizeof(buf),
+                    "kernel=persist steps_per_block=%d tiles=%dx%d tile=%dx%d cooperative=1 "
+                    "halo=%s",
+                    h->pk, h->pntx, h->pnty, persist_tile_cols(h->pk), h->pth,
+                    h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl");
+      h->plan_text = buf;
+    }
   }
   if (std::getenv("SW2D_VERBOSE")) {
     if (h->tb_k)
@@ -782,6 +836,8 @@ void free_all(sw2d* h) {
     q = nullptr;
   }
   cudaFree(h->sync);
+  cudaFree(h->pflags);
+  cudaFree(h->ppart);
   for (cudaEvent_t& e : h->ev_x)
     if (e) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b)
@@ -1032,6 +1088,13 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     }
   }
   plan_launches(h);
+  if (h->pk) {
+    const size_t nt = (size_t)h->pntx * (size_t)h->pnty;
+    const size_t fw = persist_flag_words((int)nt);
+    CUDA_TRY(h, cudaMalloc(&h->pflags, fw * sizeof(unsigned)));
+    CUDA_TRY(h, cudaMemsetAsync(h->pflags, 0, fw * sizeof(unsigned), h->stream));
+    CUDA_TRY(h, cudaMalloc(&h->ppart, nt * kPersistRedChunk * sizeof(RedPartial)));
+  }
   // reduction scratch
   long long cap = std::max<long long>(h->step_blocks, 2LL * h->step_blocks2);
   for (const Slab& s : h->slabs) {
@@ -1468,6 +1531,53 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       h->cur = 1 - h->cur;
       h->steps += k;
       left -= k;
+    }
+    return SW2D_OK;
+  }
+  if (h->pk) {  // small grids: the persistent cooperative kernel
+    Slab& sl = h->slabs[0];
+    while (nsteps > 0) {
+      const int64_t chunk =
+          std::min<int64_t>(nsteps, h->red_level ? kPersistRedChunk : (int64_t)1 << 30);
+      PersistArgs a{};
+      for (int b = 0; b < 2; ++b) {
+        a.E[b] = sl.E[b];
+        a.U[b] = sl.U[b];
+        a.V[b] = sl.V[b];
+      }
+      a.H0 = sl.H0;
+      a.pitch = h->pitch;
+      a.jbase = sl.j0 + 1 - kHaloRows;
+      a.nx = (int)h->p.nx;
+      a.ny = (int)h->p.ny;
+      a.th = h->pth;
+      a.ntx = h->pntx;
+      a.nty = h->pnty;
+      a.cur = h->cur;
+      a.nsteps = (int)chunk;
+      a.flags = h->pflags;
+      a.flag_base = h->pbase;
+      a.c = h->coef;
+      a.part = h->ppart;
+      if (h->red_level) {
+        set_dstep<<<1, 1, 0, h->stream>>>(h->dstep, (unsigned long long)h->steps);
+        h->nlaunch++;
+      }
+      const int e = launch_persist(a, h->pk, h->red_level, h->stream);
+      if (e) return fail(h, SW2D_ECUDA, std::string("cooperative launch: ") +
+                                            cudaGetErrorString((cudaError_t)e));
+      h->nlaunch++;
+      if (h->red_level) {
+        launch_fold_steps(h->ppart, h->pntx * h->pnty, (int)chunk, h->hist, h->hist_len,
+                          h->dstep, h->h0sum, (double)h->p.dx * (double)h->p.dy, h->stream);
+        h->nlaunch++;
+      }
+      CUDA_TRY(h, cudaGetLastError());
+      const int64_t blocks = (chunk + h->pk - 1) / h->pk;
+      h->cur ^= (int)(blocks & 1);
+      h->pbase += (unsigned)chunk;
+      h->steps += chunk;
+      nsteps -= chunk;
     }
     return SW2D_OK;
   }

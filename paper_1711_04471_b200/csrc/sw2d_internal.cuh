@@ -30,6 +30,8 @@ constexpr int kColsPerStrip = 4 * kOutLanes;   // 120 output columns per warp st
 // (reading R12).
 struct Coef {
   float cgx, cgy, cx, cy, q, hmin;
+  float nz;  // -0.0f: the addend of the packed products (a kernel parameter, so
+             // ptxas cannot fold fma(a, b, -0) into a multiply and contract it)
 };
 
 // One slab's fields: state n (read) and state n+1 (written).
@@ -215,6 +217,33 @@ struct TbArgs {
 };
 size_t tb_smem_bytes(int tw, int th, int K);
 void launch_tb(const TbArgs& a, void* stream);
+
+// Persistent cooperative kernel for small grids (sw2d_persist.cu): one launch
+// advances a whole grid `nsteps` steps; CTA t owns tile t (ntx x nty tiles of
+// (64 - 4K) x th cells), K steps per shared-memory block, neighbour tiles
+// synchronised through per-tile step counters.
+struct PersistArgs {
+  float* E[2];
+  float* U[2];
+  float* V[2];
+  const float* H0;
+  long long pitch;
+  long long jbase;           // global 1-based row of storage row 0
+  int nx, ny;
+  int th;                    // tile rows
+  int ntx, nty;              // tiles across / down
+  int cur;                   // buffer holding the state at the first step
+  int nsteps;
+  unsigned* flags;           // per tile: steps published (monotone across launches)
+  unsigned flag_base;        // the value every flag reached before this launch
+  Coef c;
+  RedPartial* part;          // [nsteps][ntiles] per-step CTA partials (RED >= 1)
+};
+size_t persist_smem_bytes(int K, int th);
+int persist_tile_cols(int K);
+size_t persist_flag_words(int ntiles);   // flag array length (one 128-byte line per tile)
+int persist_capacity(int K, int red_level, int th);   // co-resident CTAs
+int launch_persist(const PersistArgs& a, int K, int red_level, void* stream);  // 0 or cudaError
 
 // wet mask of the current state into a dense uint8 [nrows][nx] buffer.
 void launch_wet(const float* E, const float* H0, long long pitch,

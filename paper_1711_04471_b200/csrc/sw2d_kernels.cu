@@ -295,11 +295,13 @@ using Win = WinT<4>;
 
 struct Ctx {
   float cgx, cgy, cx, cy, q, hmin;
+  float nz;          // -0.0f, opaque to ptxas (Coef::nz; see vmul2)
   unsigned colmask;  // columns 1..nx of this lane's four
   unsigned umask;    // columns 1..nx-1 (faces that are not the east wall)
   float cmf[4];      // colmask as 1.0 / 0.0 per column
   float umf[4];      // umask as 1.0 / 0.0 per column
   float cgxc[4];     // cgx on faces that are not walls (umask), 0 on wall / outside faces
+  float hminc[4];    // hmin on columns 1..nx, +inf outside (those cells are dry)
   int ny, ra, rb;    // global rows (1-based): grid rows, this segment's output rows
   bool out_lane;
   int col;                 // storage column of this lane's element 0 (REMOTE only)
@@ -341,9 +343,25 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 // Wet/dry face rule (reading R4): the face between a cell with wet flag wc
 // and its east/north neighbour (wn) carries flow iff
 // wc ? (wn || d > 0) : (wn && d < 0); a blocked face gets 0.
-__device__ __forceinline__ bool face_flow(bool wc, bool wn, float d) {
-  return (wc & (wn | (d > 0.0f))) | (wn & (d < 0.0f));
+// face_flow(wc != 0, wn != 0, d) ? s : 0 for float wet flags, written as the
+// predicate program the rule is (two compares with a predicate combine, one
+// 3-input predicate op, one select); ptxas otherwise if-converts it into a
+// chain of selects
+__device__ __forceinline__ float face_sel(float wc, float wn, float d, float s) {
+  float r;
+  asm("{\n\t.reg .pred pc, pn, pa, pb;\n\t"
+      "setp.ne.f32 pc, %1, 0f00000000;\n\t"
+      "setp.ne.f32 pn, %2, 0f00000000;\n\t"
+      "setp.gt.or.f32 pa, %3, 0f00000000, pn;\n\t"
+      "setp.lt.and.f32 pb, %3, 0f00000000, pn;\n\t"
+      "and.pred pa, pa, pc;\n\t"
+      "or.pred pa, pa, pb;\n\t"
+      "selp.f32 %0, %4, 0f00000000, pa;\n\t}"
+      : "=f"(r)
+      : "f"(wc), "f"(wn), "f"(d), "f"(s));
+  return r;
 }
+
 
 // Column-parallel FP32 arithmetic on C-column arrays.  sm_100a issues the
 // packed add/sub/mul.rn.f32x2 (SASS FADD2 / FMUL2) at the scalar instruction
@@ -365,7 +383,7 @@ __device__ __forceinline__ bool face_flow(bool wc, bool wn, float d) {
 // SW2D_F32X2_MIN_RED (without diagnostics the packed form
 // measured slower on C3 and p2000)
 #ifndef SW2D_F32X2_MIN_RED
-#define SW2D_F32X2_MIN_RED 1
+#define SW2D_F32X2_MIN_RED 0
 #endif
 #ifndef SW2D_F32X2_SHIFTED
 #define SW2D_F32X2_SHIFTED 0
@@ -383,10 +401,46 @@ __device__ __forceinline__ void vsub2(float& d0, float& d1, float a0, float a1, 
                                       float b1) {
   SW2D_PAIR_ASM("sub.rn.f32x2");
 }
+// Packed products as fma.rn.f32x2 with a -0 addend: a*b + (-0) rounds once
+// exactly like mul.rn (the sign of a zero product included).  The -0 comes
+// from a kernel parameter (Coef::nz) so ptxas cannot fold the FMA back into a
+// multiply — it contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under
+// --fmad=false (one rounding instead of two), and it does the same to an FMA
+// whose addend it knows is -0.  An FMA is never fused with the add that
+// consumes it.  SW2D_PACKED_MUL=0 keeps the products scalar.
+#ifndef SW2D_PACKED_MUL
+#define SW2D_PACKED_MUL 1
+#endif
 __device__ __forceinline__ void vmul2(float& d0, float& d1, float a0, float a1, float b0,
-                                      float b1) {
+                                      float b1, float nz) {
+#if SW2D_PACKED_MUL && SW2D_F32X2
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mov.b64 rc, {%6,%6};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(nz));
+#else
   d0 = __fmul_rn(a0, b0);
   d1 = __fmul_rn(a1, b1);
+#endif
+}
+template <int C, bool P = true>
+__device__ __forceinline__ void vmul(float (&d)[C], const float (&a)[C], const float (&b)[C],
+                                     float nz) {
+#pragma unroll
+  for (int c = 0; c < C; c += ((SW2D_F32X2 && P) ? 2 : 1)) {
+    if (SW2D_F32X2 && P && c + 1 < C)
+      vmul2(d[c], d[c + 1], a[c], a[c + 1], b[c], b[c + 1], nz);
+    else
+      d[c] = __fmul_rn(a[c], b[c]);
+  }
+}
+template <int C, bool P = true>
+__device__ __forceinline__ void vmul(float (&d)[C], const float a, const float (&b)[C],
+                                     float nz) {
+  float aa[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) aa[c] = a;
+  vmul<C, P>(d, aa, b, nz);
 }
 #undef SW2D_PAIR_ASM
 
@@ -448,7 +502,6 @@ __device__ __forceinline__ void vselfma(float (&d)[C], const float (&w)[C], cons
   }
 SW2D_PAIR_OP(vadd, __fadd_rn)
 SW2D_PAIR_OP(vsub, __fsub_rn)
-SW2D_PAIR_OP(vmul, __fmul_rn)
 #undef SW2D_PAIR_OP
 
 // One loaded row L: reads the window `w` (rows L-1, L-2), writes `o`.
@@ -494,7 +547,8 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float hL[C], wL[C];
   vadd<C, kPack>(hL, h0L, eL);
 #pragma unroll
-  for (int c = 0; c < C; ++c) wL[c] = (rowok && !(hL[c] < x.hmin)) ? x.cmf[c] : 0.0f;
+  for (int c = 0; c < C; ++c)   // hminc: hmin on columns 1..nx, +inf outside (never <= finite h)
+    wL[c] = (rowok && !(hL[c] < x.hminc[c])) ? 1.0f : 0.0f;
   const float eR = __shfl_down_sync(kFull, eL[0], 1);
   const float hR = __shfl_down_sync(kFull, hL[0], 1);
   const float wR = __shfl_down_sync(kFull, wL[0], 1);
@@ -518,17 +572,16 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   float cg[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) cg[c] = x.cgxc[c];
-  vmul<C, kPack>(du, cg, du);
+  vmul<C, kPack>(du, cg, du, x.nz);
   vsub<C, kPack>(dv, eL, w.e);
-  vmul<C, kPack>(dv, x.cgy, dv);
+  vmul<C, kPack>(dv, x.cgy, dv, x.nz);
   vadd<C, kPack>(su, uL, du);
   vadd<C, kPack>(sv, w.v, dv);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float wn = (c < C - 1) ? wL[c + 1] : wR;
-    un[c] = face_flow(wL[c] != 0.0f, wn != 0.0f, du[c]) ? su[c] : 0.0f;
-    const bool fv = face_flow(w.w1[c] != 0.0f, wL[c] != 0.0f, dv[c]);
-    vn[c] = (vrow && fv) ? sv[c] : 0.0f;
+    un[c] = face_sel(wL[c], wn, du[c], su[c]);
+    vn[c] = vrow ? face_sel(w.w1[c], wL[c], dv[c], sv[c]) : 0.0f;
   }
 
   // a3: fluxes of row L-1 and etan(L-1)
@@ -538,23 +591,23 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     hx[c] = w.un[c] > 0.0f ? w.h[c] : ((c < C - 1) ? w.h[c + 1] : w.hR);
     hy[c] = vn[c] > 0.0f ? w.h[c] : hL[c];
   }
-  vmul<C, kPack>(fx, w.un, hx);
-  vmul<C, kPack>(fy, vn, hy);
+  vmul<C, kPack>(fx, w.un, hx, x.nz);
+  vmul<C, kPack>(fy, vn, hy, x.nz);
   const float fxw = __shfl_up_sync(kFull, fx[C - 1], 1);
   float fw[C], t[C], t2[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) fw[c] = (c > 0) ? fx[c - 1] : fxw;
   vsub<C, kPackS>(t, fx, fw);
-  vmul<C, kPack>(t, x.cx, t);
+  vmul<C, kPack>(t, x.cx, t, x.nz);
   vsub<C, kPack>(t, w.e, t);
   vsub<C, kPack>(t2, fy, w.fy);
-  vmul<C, kPack>(t2, x.cy, t2);
+  vmul<C, kPack>(t2, x.cy, t2, x.nz);
   vsub<C, kPack>(et, t, t2);
 
   // a4 (second half): E'(L-2) = wet ? A + q*(sel(wN, etan(L-1)) + sS) : etan(L-2)
   float En[C], t3[C];
   vselfma<C, kPack>(t3, w.w1, et, w.sS);   // sel(wN, etan(L-1)) + sS
-  vmul<C, kPack>(t3, x.q, t3);
+  vmul<C, kPack>(t3, x.q, t3, x.nz);
   vadd<C, kPack>(t3, w.A, t3);
 #pragma unroll
   for (int c = 0; c < C; ++c) En[c] = (w.w2[c] != 0.0f) ? t3[c] : w.etC[c];
@@ -573,14 +626,14 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   vadd<C, kPackS>(sc, wE, wW);
   vadd<C, kPack>(sc, sc, wL);
   vadd<C, kPack>(sc, sc, w.w2);
-  vmul<C, kPack>(sc, x.q, sc);
+  vmul<C, kPack>(sc, x.q, sc, x.nz);
   vsub<C, kPack>(sc, 1.0f, sc);
-  vmul<C, kPack>(t1, sc, et);
-  vmul<C, kPack>(xW, wW, eW);
+  vmul<C, kPack>(t1, sc, et, x.nz);
+  vmul<C, kPack>(xW, wW, eW, x.nz);
   vselfma<C, kPackS>(xE, wE, eE, xW);      // sel(wE, etanE) + sel(wW, etanW)
-  vmul<C, kPack>(xE, x.q, xE);
+  vmul<C, kPack>(xE, x.q, xE, x.nz);
   vadd<C, kPack>(o.A, t1, xE);
-  vmul<C, kPack>(o.sS, w.w2, w.etC);
+  vmul<C, kPack>(o.sS, w.w2, w.etC, x.nz);
 
   // a5: commit (lanes 1..30, rows of this segment)
   if (x.out_lane) {
@@ -766,7 +819,8 @@ __global__ void __launch_bounds__(32 * kStepWarps)
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-    x.q = a.c.q; x.hmin = a.c.hmin;
+    for (int c = 0; c < 4; ++c) x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
+    x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
 #ifdef SW2D_DEBUG_BOUNDS
@@ -976,7 +1030,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-    x.q = a.c.q; x.hmin = a.c.hmin;
+    for (int c = 0; c < 4; ++c) x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
+    x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
 #ifdef SW2D_DEBUG_BOUNDS
@@ -1040,7 +1095,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 
 // --- Two steps per pass (the CTA ring kernel, single slab) ------------------
 #ifndef SW2D_CTA2_PIPE
-#define SW2D_CTA2_PIPE 1      // second march one row behind (A/B builds: 0)
+#define SW2D_CTA2_PIPE 2      // second march one row behind (A/B builds: 0, 1)
 #endif
 #ifndef SW2D_CTA2_UNROLL3
 #define SW2D_CTA2_UNROLL3 1   // (without PIPE) 0: the two-row loop
@@ -1307,7 +1362,9 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       }
       x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
       for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-      x.q = a.c.q; x.hmin = a.c.hmin;
+      for (int c = 0; c < 4; ++c)
+        x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
+      x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
       x.ny = (int)a.ny;
       x.out_lane = (lane >= 1) && (lane <= kOutLanes);
       x.col = c0;
@@ -1354,6 +1411,38 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       float vC[4] = {0.f, 0.f, 0.f, 0.f};
       float e1[4] = {0.f, 0.f, 0.f, 0.f};
       // the second march writes u'(L-3), v'(L-4), eta'(L-5)
+#if SW2D_CTA2_PIPE == 2
+      // per row: march 2 (row L-3, from the slots) first, then the row's
+      // fetch straight into the hzero slot it just consumed (no copy; the
+      // shared-memory loads run under march 2's arithmetic), then march 1
+      auto phase = [&](Win2<4>& w, Win2<4>& ow, int ii, long long o, float (&uS)[4],
+                       float (&hS)[4], const float (&vIn)[4], float (&vOut)[4]) {
+        const int L = first + ii;
+        row_stepC<RED, REMOTE, 4, true>(w.s2, ow.s2, e1, hS, uS, vIn, L - 3, x, acc2, Un + o,
+                                        Vn + o - pitch, En + o - 2 * pitch);
+        float4 E4, H4, U4, V4;
+        fetch(ii, E4, H4, U4, V4);
+        const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
+        const float uL[4] = {U4.x, U4.y, U4.z, U4.w};
+        const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
+        hS[0] = H4.x; hS[1] = H4.y; hS[2] = H4.z; hS[3] = H4.w;
+        RowOut<4> r1;
+        row_stepC<RED, false, 4, false>(w.s1, ow.s1, eL, hS, uL, vL, L, x, acc1, nullptr,
+                                        nullptr, nullptr, &r1);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uS[c] = r1.un[c];
+          vOut[c] = r1.vn[c];
+          e1[c] = r1.En[c];
+        }
+      };
+      for (; i + 2 < n; i += 3) {
+        const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
+        phase(wa, wb, i, o, uA, hA, vB, vA);
+        phase(wb, wc, i + 1, o + pitch, uB, hB, vC, vB);
+        phase(wc, wa, i + 2, o + 2 * pitch, uC, hC, vA, vC);
+      }
+#else
       for (; i + 2 < n; i += 3) {
         float4 E4, H4, U4, V4;
         const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
@@ -1367,6 +1456,7 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
         row_step2p<RED, REMOTE>(wc, wa, E4, H4, U4, V4, first + i + 2, x, acc1, acc2,
                                 Un + o + 2 * pitch, Vn + o + pitch, En + o, uC, hC, vA, vC, e1);
       }
+#endif
       for (; i < n; ++i) {   // 0..2 remaining rows: shift the slots instead
         float4 E4, H4, U4, V4;
         const long long o = lo + (long long)(i - 3) * pitch;
@@ -1508,7 +1598,8 @@ __global__ void __launch_bounds__(32 * kSmallWarps)
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-    x.q = a.c.q; x.hmin = a.c.hmin;
+    for (int c = 0; c < 4; ++c) x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
+    x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 1) && (lane <= kOutLanes);
 #ifdef SW2D_DEBUG_BOUNDS
@@ -1594,7 +1685,8 @@ __global__ void __launch_bounds__(32 * kSmallWarps, SW2D_SMALL2_MINB)
     }
     x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
     for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-    x.q = a.c.q; x.hmin = a.c.hmin;
+    for (int c = 0; c < 4; ++c) x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
+    x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
     x.ny = (int)a.ny;
     x.out_lane = (lane >= 2) && (lane <= 29);
 #ifdef SW2D_DEBUG_BOUNDS

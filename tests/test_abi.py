@@ -45,21 +45,65 @@ def test_built_for_sm100a(lib):
     assert "sm_100a" in out
 
 
-def test_step_kernels_have_no_fused_multiply_add(lib):
-    """Bitwise parity needs every product rounded before its add (DESIGN.md
-    §7, packed FP32 adds): ptxas 12.9 contracts a packed f32x2 mul feeding a
-    packed add into FFMA2 even under --fmad=false, so check the SASS of the
-    2DSW step kernels for any FFMA / FFMA2."""
+def _probe_sass(red, *defines):
+    """SASS of sw2d_step_cta2<red, 0> alone (tools/cta2_probe.cu), built with the
+    library's flags plus `defines`."""
+    import subprocess
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        cubin = os.path.join(d, "probe.cubin")
+        from paper_1711_04471_b200 import _build
+        cmd = [_build.NVCC, *[f for f in _build.FLAGS if f not in ("-shared",)],
+               "-Xcompiler", "-fPIC", f"-DPROBE_RED={red}", *defines,
+               "-I", os.path.join(ROOT, "include"), "-I", _build.CSRC, "-cubin", "-o", cubin,
+               os.path.join(ROOT, "tools", "cta2_probe.cu")]
+        cmd = [c for c in cmd if c != "-Xcompiler,-fPIC,-O2,-Wall"]
+        subprocess.run(cmd, check=True, capture_output=True)
+        sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", cubin],
+                              capture_output=True, text=True).stdout
+    funcs = [f for f in re.split(r"\n\s+Function : ", sass)[1:]
+             if "sw2d_step_cta2" in f.split("\n", 1)[0]]
+    assert len(funcs) == 1
+    return funcs[0]
+
+
+@pytest.mark.parametrize("red", [0, 1, 2])
+def test_step_kernel_fuses_no_rounded_product(red):
+    """Bitwise parity needs every rounded product rounded before its add
+    (R24).  ptxas 12.9 contracts mul.rn.f32x2 + add.rn.f32x2
+    into FFMA2 even under --fmad=false, so the packed products are written as
+    fma.rn.f32x2 with a -0 addend held in a kernel parameter (Coef::nz); the
+    only other fused multiply-adds are the exact wet-flag products
+    (sel(w, x) + y, SW2D_EXACT_FMA).  With those built as mul + add
+    (SW2D_EXACT_FMA=0) every FFMA2 of the two-step kernel must be a product
+    with a scalar-broadcast addend (the -0) and no negated operand, and no
+    scalar FFMA may remain: ptxas fused nothing on its own.  (The GPU parity
+    tests, bitwise against the oracle, are the final word.)  With the products scalar too
+    (SW2D_PACKED_MUL=0) there is no fused multiply-add at all."""
+    f = _probe_sass(red, "-DSW2D_EXACT_FMA=0", "-DSW2D_F32X2_MIN_RED=0")
+    assert not re.search(r"\bFFMA\b", f), "scalar FFMA: a contracted mul + add"
+    addends = re.findall(r"\bFFMA2\s+[^;]*,\s*(-?R\d+(?:\.reuse)?\.F32\S*)\s*;", f)
+    n = len(re.findall(r"\bFFMA2\b", f))
+    assert n > 0, "packed products missing"
+    assert len(addends) == n, "an FFMA2 whose addend is not a scalar broadcast"
+    # a product with a -0 addend negates nothing; the one add with a broadcast
+    # constant in the step (1 - q*s) is a subtraction, so contracting it (or
+    # any e - t*c) would show a negated operand
+    for m in re.finditer(r"\bFFMA2\s+([^;]*);", f):
+        assert "-R" not in m.group(1), m.group(0)
+    g = _probe_sass(red, "-DSW2D_EXACT_FMA=0", "-DSW2D_PACKED_MUL=0")
+    assert not re.search(r"\bFFMA2?\b", g), "fused multiply-add with scalar products"
+
+
+def test_step_kernels_pack_adds(lib):
     import subprocess
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", sw2d._LIB_PATH],
                           capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", sass)[1:]
     steps = [f for f in funcs if "sw2d_step" in f.split("\n", 1)[0]]
     assert steps, "no sw2d_step kernels found in the SASS"
-    for f in steps:
-        name = f.split("\n", 1)[0].strip()
-        assert not re.search(r"\bFFMA2?\b", f), f"fused multiply-add in {name}"
     assert any(re.search(r"\bFADD2\b", f) for f in steps), "packed adds missing"
+    assert any(re.search(r"\bFFMA2\b", f) for f in steps), "packed products missing"
 
 
 @pytest.mark.parametrize("ny,p",[(10, 1), (17, 2), (100, 3), (16384 * 8, 8), (16, 2)])

@@ -42,7 +42,7 @@ def _cfg():
     return dict(si.config("c3"), nx=333, ny=260, sigma=12.0, seed=77)
 
 
-def _worker(rank, world, port, nsteps, halo, out_dir):
+def _worker(rank, world, port, nsteps, halo, out_dir, boot=0):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -60,8 +60,12 @@ def _worker(rank, world, port, nsteps, halo, out_dir):
         mask = (1 << sw2d.SW2D_RED_N) - 1
         p = sw2d.make_params(nx, ny, cfg["dx"], cfg["dy"], cfg["dt"], cfg["g"], cfg["eps"],
                              cfg["hmin"], reduce_every_step=mask, history_len=nsteps)
-        h = sw2d.sw2d_create(p, sw2d.make_dist(rank, world, rank, 0, obj[0], halo))
+        h = sw2d.sw2d_create(p, sw2d.make_dist(rank, world, rank, 0, obj[0], halo, boot))
         try:
+            if boot == sw2d.SW2D_BOOT_EXTERNAL:   # no NCCL: the blobs travel over torch
+                blobs = [None] * world
+                dist.all_gather_object(blobs, sw2d.sw2d_p2p_export(h))
+                sw2d.sw2d_p2p_import(h, blobs)
             sw2d.sw2d_set_state(h, *st)
             sw2d.sw2d_step(h, nsteps)
             e, u, v, w = sw2d.get_state(h, nx)
@@ -75,12 +79,14 @@ def _worker(rank, world, port, nsteps, halo, out_dir):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs two GPUs (one process per GPU)")
-@pytest.mark.parametrize("halo", [sw2d.SW2D_HALO_NCCL, sw2d.SW2D_HALO_P2P])
-def test_two_real_ranks_bitwise(halo, tmp_path):
+@pytest.mark.parametrize("halo,boot", [(sw2d.SW2D_HALO_NCCL, sw2d.SW2D_BOOT_NCCL),
+                                       (sw2d.SW2D_HALO_P2P, sw2d.SW2D_BOOT_NCCL),
+                                       (sw2d.SW2D_HALO_P2P, sw2d.SW2D_BOOT_EXTERNAL)])
+def test_two_real_ranks_bitwise(halo, boot, tmp_path):
     import torch.multiprocessing as mp
     world, nsteps = 2, 37
-    mp.spawn(_worker, args=(world, _free_port(), nsteps, halo, str(tmp_path)), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), nsteps, halo, str(tmp_path), boot),
+             nprocs=world, join=True)
     cfg = _cfg()
     st = si.generate(cfg)
     want = oracle.run(P, *st, nsteps, history=True)

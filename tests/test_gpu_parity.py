@@ -723,3 +723,63 @@ def test_legacy_default_stream_long_run():
     finally:
         sw2d.sw2d_destroy(h)
     assert_state_equal(got, want, where="legacy stream")
+
+
+# --- persistent cooperative kernel for the paper's small grids (NEXT-2) ------
+
+@pytest.mark.parametrize("k", ["1", "2"])
+@pytest.mark.parametrize("nx,ny,n,th", [(100, 100, 100, None), (500, 500, 100, None),
+                                        (263, 97, 51, "8"), (57, 300, 20, "4"),
+                                        (1, 9, 25, None), (9, 1, 25, None), (3, 3, 7, None),
+                                        (1000, 1000, 16, None), (130, 61, 33, "24")])
+def test_persistent_kernel_bitwise(nx, ny, n, th, k, monkeypatch):
+    """One cooperative launch advances the whole grid: every CTA keeps its
+    tile in shared memory, K steps per block, neighbour tiles synchronised by
+    per-tile counters (no grid barrier, no relaunch).  Bitwise equal to the
+    oracle on ragged grids and degenerate ones, with all per-step
+    diagnostics (deferred fold), chunked calls continuing the counters."""
+    monkeypatch.setenv("SW2D_PERSIST", "1")
+    monkeypatch.setenv("SW2D_PERSIST_K", k)
+    if th:
+        monkeypatch.setenv("SW2D_PERSIST_TH", th)
+    st = (si.generate(si.config("c1")) if (nx, ny) == (100, 100) else
+          si.generate(si.config("c2")) if (nx, ny) == (500, 500) else
+          _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny))
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, launches = gpu_run(P, st, n, reduce_mask=ALL)
+    assert_state_equal(got, want[:4], where=f"persistent K={k} {nx}x{ny}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    _check_history(hist, want[4], n)
+    got2, _, _, _ = gpu_run(P, st, n, chunks=[1, n // 2, n - 1 - n // 2])
+    assert_state_equal(got2, want[:4], where=f"persistent K={k} chunked")
+
+
+def test_persistent_kernel_is_the_small_grid_plan(monkeypatch):
+    """With SW2D_PERSIST=1 the planner picks the persistent kernel for the
+    paper's sizes on one GPU without ranks, the row-march kernels otherwise."""
+    monkeypatch.setenv("SW2D_PERSIST", "1")
+    h = sw2d.sw2d_create(sw2d.make_params(500, 500))
+    try:
+        assert "kernel=persist" in sw2d.sw2d_plan(h), sw2d.sw2d_plan(h)
+    finally:
+        sw2d.sw2d_destroy(h)
+    for dist in (sw2d.make_dist(0, 2, virtual_ranks=1), None):
+        nx = 500 if dist is not None else 8192
+        h = sw2d.sw2d_create(sw2d.make_params(nx, 500), dist)
+        try:
+            assert "kernel=persist" not in sw2d.sw2d_plan(h), sw2d.sw2d_plan(h)
+        finally:
+            sw2d.sw2d_destroy(h)
+
+
+@pytest.mark.parametrize("history_len", [1, 37, 300])
+def test_persistent_kernel_long_run_history(history_len, monkeypatch):
+    """C2-shaped run over several red chunks (64 steps per launch with
+    diagnostics) with the ring shorter and longer than the run."""
+    monkeypatch.setenv("SW2D_PERSIST", "1")
+    st = si.generate(si.config("c2"))
+    n = 257
+    want = oracle_run(P, st, n, history=True)
+    got, hist = _history_run(st, [3, 254], ALL, history_len)
+    assert_state_equal(got, want[:4], where=f"persistent long run, history {history_len}")
+    _check_history(hist, want[4], n)
