@@ -330,11 +330,15 @@ void plan_tb(sw2d* h, int sms) {
 }
 
 
-// Small grids (the paper's 500^2, 1000^2): the persistent cooperative kernel
-// (sw2d_persist.cu), on one GPU without ranks, if its tiles fit co-resident.
-// Tile rows: the smallest of the candidates whose tiles all fit (more tiles,
-// more parallelism), SW2D_PERSIST_TH overrides; K = 2 steps per block
-// (SW2D_PERSIST_K).  SW2D_PERSIST=0: the graph-replayed small kernels.
+// Small grids: the persistent cooperative kernel (sw2d_persist.cu), on one
+// GPU without ranks, if its tiles fit co-resident.  By default where it
+// measured faster than the graph-replayed row march: up to
+// 2^18 cells without per-step diagnostics (C1 1.55 vs 2.65 us/step, C2 3.58
+// vs 3.68), up to 2^16 with them; SW2D_PERSIST=0/1 forces it off/on (on: up
+// to 2^21 cells).  K = 2 steps per block (SW2D_PERSIST_K); tile rows
+// th = 16 rw - 4K with rw (rows per thread, 1..3; SW2D_PERSIST_RW) chosen to
+// minimise rw x (ceil(tiles / SMs) + 1) / 2 — a second CTA on an SM overlaps
+// the first one's latency (measured: C2 rw 2 on 189 tiles beats rw 3 on 117).
 constexpr int kPersistRedChunk = 64;   // steps per launch when diagnostics are folded
 void plan_persist(sw2d* h) {
   h->pk = 0;
@@ -342,29 +346,34 @@ void plan_persist(sw2d* h) {
   if (h->multi || h->virt || h->p.variant != SW2D_VARIANT_FUSED || h->slabs.size() != 1) return;
   if (cells > kSmallMaxCells) return;
   const char* on = std::getenv("SW2D_PERSIST");
-  if (!on || std::atoi(on) == 0) return;   // opt-in until it beats the graphs
-  // a forced kernel kind or the temporal-blocking experiment (tests, A/B) wins
-  if (!on && (std::getenv("SW2D_STEP_KERNEL") || h->tb_k)) return;
+  if (on && std::atoi(on) == 0) return;
+  if (!on) {   // the default: where it wins; a forced kernel kind (tests, A/B) wins too
+    if (std::getenv("SW2D_STEP_KERNEL") || h->tb_k) return;
+    if (cells > (h->red_level ? (1LL << 16) : (1LL << 18))) return;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
   int K = 2;
   if (const char* e = std::getenv("SW2D_PERSIST_K")) K = std::atoi(e) == 1 ? 1 : 2;
+  int rw_force = 0;
+  if (const char* e = std::getenv("SW2D_PERSIST_RW")) rw_force = std::max(1, std::min(3, std::atoi(e)));
   const int tw = persist_tile_cols(K);
   const int ntx = (int)((h->p.nx + tw - 1) / tw);
-  static const int cand[] = {4, 8, 12, 16, 24, 32, 48, 64, 96, 128};
-  int th_force = 0;
-  if (const char* e = std::getenv("SW2D_PERSIST_TH")) th_force = std::max(1, std::atoi(e));
-  for (int th : cand) {
-    if (th_force) th = th_force;
-    if (persist_smem_bytes(K, th) > 226 * 1024) break;
+  long long best = -1;
+  for (int rw = 1; rw <= 3; ++rw) {
+    if (rw_force && rw != rw_force) continue;
+    const int th = persist_tile_rows(K, rw);
     const int nty = (int)((h->p.ny + th - 1) / th);
-    const int cap = persist_capacity(K, h->red_level, th);
-    if ((long long)ntx * nty <= cap) {
+    const long long nt = (long long)ntx * nty;
+    if (nt > persist_capacity(K, h->red_level, rw)) continue;
+    const long long cost = rw * ((nt + sms - 1) / sms + 1);
+    if (best < 0 || cost < best) {
+      best = cost;
       h->pk = K;
       h->pth = th;
       h->pntx = ntx;
       h->pnty = nty;
-      return;
     }
-    if (th_force) return;
   }
 }
 

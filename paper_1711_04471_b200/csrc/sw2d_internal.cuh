@@ -230,7 +230,7 @@ struct PersistArgs {
   long long pitch;
   long long jbase;           // global 1-based row of storage row 0
   int nx, ny;
-  int th;                    // tile rows
+  int th;                    // tile rows (16 rw - 4K)
   int ntx, nty;              // tiles across / down
   int cur;                   // buffer holding the state at the first step
   int nsteps;
@@ -239,10 +239,10 @@ struct PersistArgs {
   Coef c;
   RedPartial* part;          // [nsteps][ntiles] per-step CTA partials (RED >= 1)
 };
-size_t persist_smem_bytes(int K, int th);
 int persist_tile_cols(int K);
+int persist_tile_rows(int K, int rw);    // rw: tile rows per thread (1..3)
 size_t persist_flag_words(int ntiles);   // flag array length (one 128-byte line per tile)
-int persist_capacity(int K, int red_level, int th);   // co-resident CTAs
+int persist_capacity(int K, int red_level, int rw);   // co-resident CTAs
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream);  // 0 or cudaError
 
 // wet mask of the current state into a dense uint8 [nrows][nx] buffer.

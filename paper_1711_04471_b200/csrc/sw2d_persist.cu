@@ -38,19 +38,12 @@ namespace sw2d_dev {
 
 namespace {
 
-constexpr int kPX = 64;       // shared tile width (2 columns per lane)
-constexpr int kPThreadsY = 8; // blockDim = (32, kPThreadsY)
-constexpr int kPThreads = 32 * kPThreadsY;
+constexpr int kPX = 64;       // shared tile width: 32 lanes x 2 columns
+constexpr int kPW = 16;       // warps per CTA: warp w owns tile rows w, w + 16, ...
+constexpr int kPThreads = 32 * kPW;
 constexpr int kPFlagStride = 32;        // uints between two tiles' flags (128 B)
-constexpr int kPSmemMax = 226 * 1024;   // dynamic shared memory cap (the reduction's static buffer fits beside)
-
-__device__ __forceinline__ float p_flux(float s, float hl, float hr) {
-  return s > 0.0f ? __fmul_rn(s, hl) : (s < 0.0f ? __fmul_rn(s, hr) : 0.0f);
-}
-
-__device__ __forceinline__ bool p_flows(bool wc, bool wn, float d) {
-  return wc ? (wn || d > 0.0f) : (wn && d < 0.0f);
-}
+constexpr int kPSmemMax = 226 * 1024;   // dynamic shared memory cap (static buffers fit beside)
+constexpr unsigned kFullMask = 0xffffffffu;
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
@@ -62,78 +55,115 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// the face rule's predicate program (as in the row march): flow ? s : 0
+__device__ __forceinline__ float p_face(float wc, float wn, float d, float s) {
+  float r;
+  asm("{\n\t.reg .pred pc, pn, pa, pb;\n\t"
+      "setp.ne.f32 pc, %1, 0f00000000;\n\t"
+      "setp.ne.f32 pn, %2, 0f00000000;\n\t"
+      "setp.gt.or.f32 pa, %3, 0f00000000, pn;\n\t"
+      "setp.lt.and.f32 pb, %3, 0f00000000, pn;\n\t"
+      "and.pred pa, pa, pc;\n\t"
+      "or.pred pa, pa, pb;\n\t"
+      "selp.f32 %0, %4, 0f00000000, pa;\n\t}"
+      : "=f"(r)
+      : "f"(wc), "f"(wn), "f"(d), "f"(s));
+  return r;
+}
+
+// upwind flux s * (s > 0 ? hl : hr): equal in value to the oracle's
+// F(s, hl, hr) for finite depths (reading R22)
+__device__ __forceinline__ float p_flux(float s, float hl, float hr) {
+  return __fmul_rn(s, s > 0.0f ? hl : hr);
+}
+
 struct PAcc {
   double s;
   double wet;
   float mx, nmn, mu, mv;
 };
 
-template <int K, int RED>
+// K: steps per block; RW: tile rows per thread (the shared tile is 16 RW rows)
+template <int K, int RW, int RED>
 __global__ void __launch_bounds__(kPThreads)
     sw2d_persist(const PersistArgs a) {
   constexpr int A = 2 * K;            // apron cells per side
   constexpr int TW = kPX - 2 * A;     // tile width
+  constexpr int Y = kPW * RW;         // shared tile rows
+  constexpr int TH = Y - 2 * A;       // tile rows
+  constexpr int N = Y * kPX;
   extern __shared__ __align__(16) float psm[];
-  const int TH = a.th, Y = TH + 2 * A, N = Y * kPX;
-  float* sE = psm;        // eta (state being advanced)
-  float* sH0 = sE + N;    // hzero (static)
-  float* sU = sH0 + N;
+  float* sE = psm;        // eta (the state being advanced; U, V, H0 likewise)
+  float* sU = sE + N;
   float* sV = sU + N;
-  float* sh = sV + N;     // h
+  float* sH0 = sV + N;
+  float* sh = sH0 + N;    // h of this step
   float* sw = sh + N;     // wet flags 1/0
-  float* sun = sw + N;    // un
-  float* svn = sun + N;   // vn
+  float* svn = sw + N;    // vn (read one row up by etan)
   float* set = svn + N;   // etan
 
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int tile = blockIdx.x;
   const int tk = tile % a.ntx, tj = tile / a.ntx;
   const int gk0 = tk * TW + 1 - A;   // global 1-based column of shared column 0
   const int gj0 = tj * TH + 1 - A;   // global 1-based row of shared row 0
   const int nx = a.nx, ny = a.ny;
   const long long pitch = a.pitch;
-  const float cgx = a.c.cgx, cgy = a.c.cgy, cx = a.c.cx, cy = a.c.cy, q = a.c.q,
-              hmin = a.c.hmin;
+  const float cy = a.c.cy, cx = a.c.cx, q = a.c.q;
+  const int c0 = 2 * lane;           // this thread's columns c0, c0 + 1
 
-  // in-grid masks of this thread's two columns
-  const int x0 = 2 * tx;
-  const int gka = gk0 + x0, gkb = gka + 1;
-  const bool ina = gka >= 1 && gka <= nx, inb = gkb >= 1 && gkb <= nx;
-
+  // per-thread constants: in-grid column flags, wall-face coefficients
+  // (cgx on faces that are neither walls nor outside, 0 there: the face rule
+  // then blocks them, as for the row march), hmin or +inf outside
+  float hminc[2], cgxc[2];
+  bool colin[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int gk = gk0 + c0 + c;
+    colin[c] = gk >= 1 && gk <= nx;
+    hminc[c] = colin[c] ? a.c.hmin : __int_as_float(0x7f800000);
+    cgxc[c] = (gk >= 1 && gk < nx) ? a.c.cgx : 0.0f;
+  }
+  float cgyr[RW];
+  bool rowin[RW], rowin_n[RW];
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+    const int gj = gj0 + wp + kPW * k;
+    rowin[k] = gj >= 1 && gj <= ny;
+    rowin_n[k] = gj + 1 >= 1 && gj + 1 <= ny;
+    cgyr[k] = (gj >= 1 && gj < ny) ? a.c.cgy : 0.0f;
+  }
   auto gofs = [&](int y, int x) -> long long {
     return (long long)(gj0 + y - a.jbase) * pitch + (gk0 + x) + kColOff;
-  };
-  auto in_grid = [&](int y, int x) {
-    const int gj = gj0 + y, gk = gk0 + x;
-    return gj >= 1 && gj <= ny && gk >= 1 && gk <= nx;
   };
 
   int b = a.cur;   // buffer holding the current state
   // initial load: the whole apron'd tile (zero outside the grid)
-  for (int y = ty; y < Y; y += kPThreadsY) {
+#pragma unroll
+  for (int k = 0; k < RW; ++k) {
+    const int y = wp + kPW * k, i = y * kPX + c0;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const int x = x0 + c, i = y * kPX + x;
       float e = 0.0f, h0 = 0.0f, u = 0.0f, v = 0.0f;
-      if (in_grid(y, x)) {
-        const long long o = gofs(y, x);
+      if (rowin[k] && colin[c]) {
+        const long long o = gofs(y, c0 + c);
         e = __ldcg(a.E[b] + o);
         h0 = __ldcg(a.H0 + o);
         u = __ldcg(a.U[b] + o);
         v = __ldcg(a.V[b] + o);
       }
-      sE[i] = e;
-      sH0[i] = h0;
-      sU[i] = u;
-      sV[i] = v;
+      sE[i + c] = e;
+      sH0[i + c] = h0;
+      sU[i + c] = u;
+      sV[i + c] = v;
     }
   }
   __syncthreads();
 
   // neighbour tiles (8-neighbourhood; -1 when outside)
   int nb = -1;
-  if (tid < 9 && tid != 4) {
-    const int dj = tid / 3 - 1, dk = tid % 3 - 1;
+  if (threadIdx.x < 9 && threadIdx.x != 4) {
+    const int dj = threadIdx.x / 3 - 1, dk = threadIdx.x % 3 - 1;
     const int nj = tj + dj, nk = tk + dk;
     if (nj >= 0 && nj < a.nty && nk >= 0 && nk < a.ntx) nb = nj * a.ntx + nk;
   }
@@ -143,61 +173,75 @@ __global__ void __launch_bounds__(kPThreads)
     const int kk = min(K, a.nsteps - done);
     for (int s = 0; s < kk; ++s) {
       const int step = done + s;
-      // P1: h and wet
-      for (int y = ty; y < Y; y += kPThreadsY) {
+      // this thread's cells, kept in registers across the phases
+      float e[RW][2], u[RW][2], v[RW][2], h0[RW][2], h[RW][2], w[RW][2], un[RW][2],
+          vn[RW][2], et[RW][2];
+      // P1: h, wet; un (east faces), vn (north faces)
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int y = wp + kPW * k, i = y * kPX + c0;
+        const int iN = min(y + 1, Y - 1) * kPX + c0;   // the last row's north is stale anyway
+        const float2 e2 = *reinterpret_cast<const float2*>(sE + i);
+        const float2 h02 = *reinterpret_cast<const float2*>(sH0 + i);
+        const float2 u2 = *reinterpret_cast<const float2*>(sU + i);
+        const float2 v2 = *reinterpret_cast<const float2*>(sV + i);
+        const float2 eN2 = *reinterpret_cast<const float2*>(sE + iN);
+        const float2 h0N2 = *reinterpret_cast<const float2*>(sH0 + iN);
+        e[k][0] = e2.x; e[k][1] = e2.y;
+        h0[k][0] = h02.x; h0[k][1] = h02.y;
+        u[k][0] = u2.x; u[k][1] = u2.y;
+        v[k][0] = v2.x; v[k][1] = v2.y;
+        const float eN[2] = {eN2.x, eN2.y}, h0N[2] = {h0N2.x, h0N2.y};
+        float wN[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int x = x0 + c, i = y * kPX + x;
-          const float hv = __fadd_rn(sH0[i], sE[i]);
-          sh[i] = hv;
-          sw[i] = (in_grid(y, x) && !(hv < hmin)) ? 1.0f : 0.0f;
+          h[k][c] = __fadd_rn(h0[k][c], e[k][c]);
+          w[k][c] = (rowin[k] && !(h[k][c] < hminc[c])) ? 1.0f : 0.0f;
+          const float hN = __fadd_rn(h0N[c], eN[c]);
+          wN[c] = (rowin_n[k] && !(hN < hminc[c])) ? 1.0f : 0.0f;
         }
-      }
-      __syncthreads();
-      // P2: face velocities (walls and faces outside the grid: 0)
-      for (int y = ty; y < Y; y += kPThreadsY) {
-        const int gj = gj0 + y;
-        const bool rin = gj >= 1 && gj <= ny;
+        // east neighbours: column c0 + 2 is the next lane's first
+        const float eE1 = __shfl_down_sync(kFullMask, e[k][0], 1);
+        const float wE1 = __shfl_down_sync(kFullMask, w[k][0], 1);
+        const float eE[2] = {e[k][1], eE1}, wE[2] = {w[k][1], wE1};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int x = x0 + c, i = y * kPX + x;
-          const int gk = gk0 + x;
-          float u = 0.0f, v = 0.0f;
-          if (rin && (c ? inb : ina)) {
-            if (gk != nx && x + 1 < kPX) {
-              const float du = __fmul_rn(cgx, __fsub_rn(sE[i + 1], sE[i]));
-              if (p_flows(sw[i] != 0.0f, sw[i + 1] != 0.0f, du)) u = __fadd_rn(sU[i], du);
-            }
-            if (gj != ny && y + 1 < Y) {
-              const float dv = __fmul_rn(cgy, __fsub_rn(sE[i + kPX], sE[i]));
-              if (p_flows(sw[i] != 0.0f, sw[i + kPX] != 0.0f, dv)) v = __fadd_rn(sV[i], dv);
-            }
-          }
-          sun[i] = u;
-          svn[i] = v;
+          const float du = __fmul_rn(cgxc[c], __fsub_rn(eE[c], e[k][c]));
+          un[k][c] = p_face(w[k][c], wE[c], du, __fadd_rn(u[k][c], du));
+          const float dv = __fmul_rn(cgyr[k], __fsub_rn(eN[c], e[k][c]));
+          vn[k][c] = p_face(w[k][c], wN[c], dv, __fadd_rn(v[k][c], dv));
         }
+        *reinterpret_cast<float2*>(sh + i) = make_float2(h[k][0], h[k][1]);
+        *reinterpret_cast<float2*>(sw + i) = make_float2(w[k][0], w[k][1]);
+        *reinterpret_cast<float2*>(svn + i) = make_float2(vn[k][0], vn[k][1]);
       }
       __syncthreads();
-      // P3: etan (the outermost ring stays stale)
-      for (int y = ty; y < Y; y += kPThreadsY) {
+      // P2: etan = (E - cx (Fe - Fw)) - cy (Fn - Fs)
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int y = wp + kPW * k;
+        const int iN = min(y + 1, Y - 1) * kPX + c0, iS = max(y - 1, 0) * kPX + c0;
+        const float2 hN2 = *reinterpret_cast<const float2*>(sh + iN);
+        const float2 hS2 = *reinterpret_cast<const float2*>(sh + iS);
+        const float2 vS2 = *reinterpret_cast<const float2*>(svn + iS);
+        const float hN[2] = {hN2.x, hN2.y}, hS[2] = {hS2.x, hS2.y}, vS[2] = {vS2.x, vS2.y};
+        const float hE1 = __shfl_down_sync(kFullMask, h[k][0], 1);
+        const float hW0 = __shfl_up_sync(kFullMask, h[k][1], 1);
+        const float uW0 = __shfl_up_sync(kFullMask, un[k][1], 1);
+        const float hE[2] = {h[k][1], hE1}, hW[2] = {hW0, h[k][0]}, uW[2] = {uW0, un[k][0]};
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int x = x0 + c, i = y * kPX + x;
-          float e = 0.0f;
-          if (x >= 1 && x + 1 < kPX && y >= 1 && y + 1 < Y) {
-            const float hc = sh[i];
-            const float fe = p_flux(sun[i], hc, sh[i + 1]);
-            const float fw = p_flux(sun[i - 1], sh[i - 1], hc);
-            const float fn = p_flux(svn[i], hc, sh[i + kPX]);
-            const float fs = p_flux(svn[i - kPX], sh[i - kPX], hc);
-            e = __fsub_rn(__fsub_rn(sE[i], __fmul_rn(cx, __fsub_rn(fe, fw))),
-                          __fmul_rn(cy, __fsub_rn(fn, fs)));
-          }
-          set[i] = e;
+          const float fe = p_flux(un[k][c], h[k][c], hE[c]);
+          const float fw = p_flux(uW[c], hW[c], h[k][c]);
+          const float fn = p_flux(vn[k][c], h[k][c], hN[c]);
+          const float fs = p_flux(vS[c], hS[c], h[k][c]);
+          et[k][c] = __fsub_rn(__fsub_rn(e[k][c], __fmul_rn(cx, __fsub_rn(fe, fw))),
+                               __fmul_rn(cy, __fsub_rn(fn, fs)));
         }
+        *reinterpret_cast<float2*>(set + y * kPX + c0) = make_float2(et[k][0], et[k][1]);
       }
       __syncthreads();
-      // P4: Shapiro filter and commit; diagnostics over the exact centre
+      // P3: Shapiro filter (wet cells), commit
       PAcc acc;
       acc.s = 0.0;
       acc.wet = 0.0;
@@ -205,78 +249,84 @@ __global__ void __launch_bounds__(kPThreads)
       acc.nmn = __int_as_float(0xff800000);
       acc.mu = 0.0f;
       acc.mv = 0.0f;
-      for (int y = ty; y < Y; y += kPThreadsY) {
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int y = wp + kPW * k, i = y * kPX + c0;
+        const int iN = min(y + 1, Y - 1) * kPX + c0, iS = max(y - 1, 0) * kPX + c0;
+        const float2 eN2 = *reinterpret_cast<const float2*>(set + iN);
+        const float2 eS2 = *reinterpret_cast<const float2*>(set + iS);
+        const float2 wN2 = *reinterpret_cast<const float2*>(sw + iN);
+        const float2 wS2 = *reinterpret_cast<const float2*>(sw + iS);
+        const float etE1 = __shfl_down_sync(kFullMask, et[k][0], 1);
+        const float etW0 = __shfl_up_sync(kFullMask, et[k][1], 1);
+        const float wE1 = __shfl_down_sync(kFullMask, w[k][0], 1);
+        const float wW0 = __shfl_up_sync(kFullMask, w[k][1], 1);
+        const float etE[2] = {et[k][1], etE1}, etW[2] = {etW0, et[k][0]};
+        const float wE[2] = {w[k][1], wE1}, wW[2] = {wW0, w[k][0]};
+        const float etN[2] = {eN2.x, eN2.y}, etS[2] = {eS2.x, eS2.y};
+        const float wN[2] = {wN2.x, wN2.y}, wS[2] = {wS2.x, wS2.y};
+        float en[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          const int x = x0 + c, i = y * kPX + x;
-          float e = 0.0f;
-          const bool in = in_grid(y, x);
-          if (in) {
-            e = set[i];
-            if (sw[i] != 0.0f && x >= 1 && x + 1 < kPX && y >= 1 && y + 1 < Y) {
-              const bool wE = sw[i + 1] != 0.0f, wW = sw[i - 1] != 0.0f;
-              const bool wN = sw[i + kPX] != 0.0f, wS = sw[i - kPX] != 0.0f;
-              const float sc = (float)((int)wE + (int)wW + (int)wN + (int)wS);
-              const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(q, sc)), e);
-              const float t2 =
-                  __fmul_rn(q, __fadd_rn(wE ? set[i + 1] : 0.0f, wW ? set[i - 1] : 0.0f));
-              const float t3 =
-                  __fmul_rn(q, __fadd_rn(wN ? set[i + kPX] : 0.0f, wS ? set[i - kPX] : 0.0f));
-              e = __fadd_rn(__fadd_rn(t1, t2), t3);
-            }
-          }
-          const float un = sun[i], vn = svn[i];
-          if (RED >= 1 && in && y >= A && y < A + TH && x >= A && x < A + TW) {
-            acc.s += (double)e;
+          // E' = ((1 - q s) etan + q (sel(wE, .) + sel(wW, .))) + q (sel(wN, .) + sel(wS, .));
+          // a select sel(w, x) + y is the exact fma(w, x, y) (R24)
+          const float sc = __fadd_rn(__fadd_rn(__fadd_rn(wE[c], wW[c]), wN[c]), wS[c]);
+          const float t1 = __fmul_rn(__fsub_rn(1.0f, __fmul_rn(q, sc)), et[k][c]);
+          const float t2 = __fmul_rn(q, __fmaf_rn(wE[c], etE[c], __fmul_rn(wW[c], etW[c])));
+          const float t3 = __fmul_rn(q, __fmaf_rn(wN[c], etN[c], __fmul_rn(wS[c], etS[c])));
+          en[c] = w[k][c] != 0.0f ? __fadd_rn(__fadd_rn(t1, t2), t3) : et[k][c];
+        }
+        *reinterpret_cast<float2*>(sE + i) = make_float2(en[0], en[1]);
+        *reinterpret_cast<float2*>(sU + i) = make_float2(un[k][0], un[k][1]);
+        *reinterpret_cast<float2*>(sV + i) = make_float2(vn[k][0], vn[k][1]);
+        if (RED >= 1 && y >= A && y < A + TH && c0 >= A && c0 < A + TW) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            if (!(rowin[k] && colin[c])) continue;
+            acc.s += (double)en[c];
             if (RED >= 2) {
-              acc.mx = fmaxf(acc.mx, e);
-              acc.nmn = fmaxf(acc.nmn, -e);
-              acc.wet += (__fadd_rn(sH0[i], e) < hmin) ? 0.0 : 1.0;
-              acc.mu = fmaxf(acc.mu, fabsf(un));
-              acc.mv = fmaxf(acc.mv, fabsf(vn));
+              acc.mx = fmaxf(acc.mx, en[c]);
+              acc.nmn = fmaxf(acc.nmn, -en[c]);
+              acc.wet += (__fadd_rn(h0[k][c], en[c]) < a.c.hmin) ? 0.0 : 1.0;
+              acc.mu = fmaxf(acc.mu, fabsf(un[k][c]));
+              acc.mv = fmaxf(acc.mv, fabsf(vn[k][c]));
             }
           }
-          // commit after everyone's reads of this step's et / un / vn: each
-          // cell's new E, U, V are written by its own thread only, and no
-          // thread reads E, U, V again before the next P1 barrier
-          sE[i] = e;
-          sU[i] = un;
-          sV[i] = vn;
         }
       }
       if (RED >= 1) {   // CTA fold of this step's partial (deferred fold_steps)
-        __shared__ PAcc red_sh[kPThreads / 32];
+        __shared__ PAcc red_sh[kPW];
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) {
-          acc.s += __shfl_xor_sync(0xffffffffu, acc.s, m);
+          acc.s += __shfl_xor_sync(kFullMask, acc.s, m);
           if (RED >= 2) {
-            acc.wet += __shfl_xor_sync(0xffffffffu, acc.wet, m);
-            acc.mx = fmaxf(acc.mx, __shfl_xor_sync(0xffffffffu, acc.mx, m));
-            acc.nmn = fmaxf(acc.nmn, __shfl_xor_sync(0xffffffffu, acc.nmn, m));
-            acc.mu = fmaxf(acc.mu, __shfl_xor_sync(0xffffffffu, acc.mu, m));
-            acc.mv = fmaxf(acc.mv, __shfl_xor_sync(0xffffffffu, acc.mv, m));
+            acc.wet += __shfl_xor_sync(kFullMask, acc.wet, m);
+            acc.mx = fmaxf(acc.mx, __shfl_xor_sync(kFullMask, acc.mx, m));
+            acc.nmn = fmaxf(acc.nmn, __shfl_xor_sync(kFullMask, acc.nmn, m));
+            acc.mu = fmaxf(acc.mu, __shfl_xor_sync(kFullMask, acc.mu, m));
+            acc.mv = fmaxf(acc.mv, __shfl_xor_sync(kFullMask, acc.mv, m));
           }
         }
-        if (tx == 0) red_sh[ty] = acc;
+        if (lane == 0) red_sh[wp] = acc;
         __syncthreads();
-        if (tid == 0) {
+        if (threadIdx.x == 0) {
           PAcc t = red_sh[0];
-          for (int w = 1; w < kPThreadsY; ++w) {
-            t.s += red_sh[w].s;
-            t.wet += red_sh[w].wet;
-            t.mx = fmaxf(t.mx, red_sh[w].mx);
-            t.nmn = fmaxf(t.nmn, red_sh[w].nmn);
-            t.mu = fmaxf(t.mu, red_sh[w].mu);
-            t.mv = fmaxf(t.mv, red_sh[w].mv);
+          for (int q2 = 1; q2 < kPW; ++q2) {
+            t.s += red_sh[q2].s;
+            t.wet += red_sh[q2].wet;
+            t.mx = fmaxf(t.mx, red_sh[q2].mx);
+            t.nmn = fmaxf(t.nmn, red_sh[q2].nmn);
+            t.mu = fmaxf(t.mu, red_sh[q2].mu);
+            t.mv = fmaxf(t.mv, red_sh[q2].mv);
           }
-          RedPartial p;
-          p.sum_eta = t.s;
-          p.wet = t.wet;
-          p.max_eta = t.mx;
-          p.neg_min_eta = t.nmn;
-          p.max_u = t.mu;
-          p.max_v = t.mv;
-          a.part[(size_t)step * gridDim.x + tile] = p;
+          RedPartial pr;
+          pr.sum_eta = t.s;
+          pr.wet = t.wet;
+          pr.max_eta = t.mx;
+          pr.neg_min_eta = t.nmn;
+          pr.max_u = t.mu;
+          pr.max_v = t.mv;
+          a.part[(size_t)step * gridDim.x + tile] = pr;
         }
       }
       __syncthreads();
@@ -284,11 +334,14 @@ __global__ void __launch_bounds__(kPThreads)
     done += kk;
     b ^= 1;
     // publish the exact centre of the new state, then the tile's counter
-    for (int y = A + ty; y < A + TH; y += kPThreadsY) {
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int y = wp + kPW * k;
+      if (y < A || y >= A + TH || !rowin[k]) continue;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int x = x0 + c;
-        if (x >= A && x < A + TW && in_grid(y, x)) {
+        const int x = c0 + c;
+        if (x >= A && x < A + TW && colin[c]) {
           const int i = y * kPX + x;
           const long long o = gofs(y, x);
           __stcg(a.E[b] + o, sE[i]);
@@ -301,7 +354,8 @@ __global__ void __launch_bounds__(kPThreads)
     __syncthreads();
     // (the barrier orders the CTA's stores before thread 0's release, which
     // is cumulative at gpu scope)
-    if (tid == 0) st_release(a.flags + (size_t)tile * kPFlagStride, a.flag_base + (unsigned)done);
+    if (threadIdx.x == 0)
+      st_release(a.flags + (size_t)tile * kPFlagStride, a.flag_base + (unsigned)done);
     // wait for the neighbours' same block (they wrote our apron and are done
     // reading the buffer we write next); each flag sits in its own 128-byte
     // line (no hot L2 slice), and the pollers back off
@@ -316,15 +370,17 @@ __global__ void __launch_bounds__(kPThreads)
     }
     __syncthreads();
     // reload the apron ring (the centre is already here)
-    for (int y = ty; y < Y; y += kPThreadsY) {
+#pragma unroll
+    for (int k = 0; k < RW; ++k) {
+      const int y = wp + kPW * k;
       const bool rowc = y >= A && y < A + TH;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int x = x0 + c;
+        const int x = c0 + c;
         if (rowc && x >= A && x < A + TW) continue;
         const int i = y * kPX + x;
         float e = 0.0f, u = 0.0f, v = 0.0f;
-        if (in_grid(y, x)) {
+        if (rowin[k] && colin[c]) {
           const long long o = gofs(y, x);
           e = __ldcg(a.E[b] + o);
           u = __ldcg(a.U[b] + o);
@@ -339,69 +395,78 @@ __global__ void __launch_bounds__(kPThreads)
   }
 }
 
-template <int K, int RED>
+template <int K, int RW, int RED>
 void persist_attr() {
   static unsigned long long attr_devices = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_devices >> (dev & 63) & 1ull)) {
     // (static + dynamic shared memory must stay within 227 KB per CTA)
-    cudaFuncSetAttribute(sw2d_persist<K, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sw2d_persist<K, RW, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kPSmemMax);
     attr_devices |= 1ull << (dev & 63);
   }
 }
 
-template <int K, int RED>
-int persist_capacity_k(int th) {
-  persist_attr<K, RED>();
+constexpr size_t smem_of(int rw) { return (size_t)8 * (size_t)(kPW * rw) * kPX * sizeof(float); }
+
+template <int K, int RW, int RED>
+int capacity_t() {
+  persist_attr<K, RW, RED>();
   int per_sm = 0, sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (persist_smem_bytes(K, th) > (size_t)kPSmemMax) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, RED>, kPThreads,
-                                                    persist_smem_bytes(K, th)) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, RW, RED>, kPThreads,
+                                                    smem_of(RW)) != cudaSuccess) {
     cudaGetLastError();   // not sticky: the planner falls back
     return 0;
   }
   return per_sm * sms;
 }
 
-template <int K, int RED>
-int launch_persist_k(const PersistArgs& a, cudaStream_t s) {
-  persist_attr<K, RED>();
+template <int K, int RW, int RED>
+int launch_t(const PersistArgs& a, cudaStream_t s) {
+  persist_attr<K, RW, RED>();
   void* args[] = {const_cast<PersistArgs*>(&a)};
-  const cudaError_t e = cudaLaunchCooperativeKernel(
-      (const void*)sw2d_persist<K, RED>, dim3((unsigned)(a.ntx * a.nty)),
-      dim3(32, kPThreadsY), args, persist_smem_bytes(K, a.th), s);
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)sw2d_persist<K, RW, RED>,
+                                                    dim3((unsigned)(a.ntx * a.nty)),
+                                                    dim3(kPThreads), args, smem_of(RW), s);
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+template <int K, int RW>
+int capacity_kr(int red) {
+  return red >= 2 ? capacity_t<K, RW, 2>() : red ? capacity_t<K, RW, 1>() : capacity_t<K, RW, 0>();
+}
+template <int K, int RW>
+int launch_kr(const PersistArgs& a, int red, cudaStream_t s) {
+  return red >= 2 ? launch_t<K, RW, 2>(a, s) : red ? launch_t<K, RW, 1>(a, s)
+                                                   : launch_t<K, RW, 0>(a, s);
 }
 
 }  // namespace
 
-size_t persist_smem_bytes(int K, int th) {
-  return (size_t)9 * (size_t)(th + 4 * K) * kPX * sizeof(float);
-}
-
+// tile rows per configuration: th = 16 RW - 4K (RW in {1, 2, 3})
+int persist_tile_rows(int K, int rw) { return kPW * rw - 4 * K; }
 int persist_tile_cols(int K) { return kPX - 4 * K; }
-
 size_t persist_flag_words(int ntiles) { return (size_t)ntiles * kPFlagStride; }
 
-int persist_capacity(int K, int red_level, int th) {
+int persist_capacity(int K, int red_level, int rw) {
   if (K == 1)
-    return red_level >= 2 ? persist_capacity_k<1, 2>(th)
-                          : red_level ? persist_capacity_k<1, 1>(th) : persist_capacity_k<1, 0>(th);
-  return red_level >= 2 ? persist_capacity_k<2, 2>(th)
-                        : red_level ? persist_capacity_k<2, 1>(th) : persist_capacity_k<2, 0>(th);
+    return rw == 1 ? capacity_kr<1, 1>(red_level) : rw == 2 ? capacity_kr<1, 2>(red_level)
+                                                           : capacity_kr<1, 3>(red_level);
+  return rw == 1 ? capacity_kr<2, 1>(red_level) : rw == 2 ? capacity_kr<2, 2>(red_level)
+                                                         : capacity_kr<2, 3>(red_level);
 }
 
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  const int rw = (a.th + 4 * K) / kPW;
   if (K == 1)
-    return red_level >= 2 ? launch_persist_k<1, 2>(a, s)
-                          : red_level ? launch_persist_k<1, 1>(a, s) : launch_persist_k<1, 0>(a, s);
-  return red_level >= 2 ? launch_persist_k<2, 2>(a, s)
-                        : red_level ? launch_persist_k<2, 1>(a, s) : launch_persist_k<2, 0>(a, s);
+    return rw == 1 ? launch_kr<1, 1>(a, red_level, s) : rw == 2 ? launch_kr<1, 2>(a, red_level, s)
+                                                               : launch_kr<1, 3>(a, red_level, s);
+  return rw == 1 ? launch_kr<2, 1>(a, red_level, s) : rw == 2 ? launch_kr<2, 2>(a, red_level, s)
+                                                             : launch_kr<2, 3>(a, red_level, s);
 }
 
 }  // namespace sw2d_dev
