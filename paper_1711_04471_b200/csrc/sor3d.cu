@@ -42,6 +42,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "sor3d.h"
 #include <nvtx3/nvToolsExt.h>
@@ -791,10 +792,16 @@ int sor3d_residual_history(sor3d* h, double* out, int64_t n) {
   SOR_ENTER(h);
   if (!out || n < 0 || n > h->nrec || n > h->cap)
     return fail(h, SOR3D_EINVAL, "n must be <= min(records, history_len)");
+  if (n == 0) return SOR3D_OK;
+  // the whole ring in one copy on the handle's stream, then index on the host
+  std::vector<double> ring(2 * (size_t)h->cap);
+  SOR_TRY(h, cudaMemcpyAsync(ring.data(), h->hist, ring.size() * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->stream));
   SOR_TRY(h, cudaStreamSynchronize(h->stream));
   for (int64_t t = 0; t < n; ++t) {
     const int64_t r = (h->nrec - n + t) % h->cap;
-    SOR_TRY(h, cudaMemcpy(out + 2 * t, h->hist + 2 * r, 2 * sizeof(double), cudaMemcpyDefault));
+    out[2 * t] = ring[2 * r];
+    out[2 * t + 1] = ring[2 * r + 1];
   }
   return SOR3D_OK;
 }

@@ -71,7 +71,6 @@ struct sw2d {
   int nstrips2 = 0;  // kind 2, two steps per launch: 56-column strips
   int64_t fault_skip_halo = -1;  // SW2D_FAULT_SKIP_HALO (tests only)
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
-  int tb_tw = 0, tb_th = 0, tb_k = 0;  // temporal blocking (small grids); tb_k = 0: off
   // persistent cooperative kernel (small grids): K steps per shared-memory
   // block, pntx x pnty tiles of pth rows, one CTA each; pk = 0: off
   int pk = 0, pth = 0, pntx = 0, pnty = 0;
@@ -305,31 +304,6 @@ int red_level_of(uint32_t mask) {
 
 float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch; }
 
-// Small grids (the paper's 500^2 runs) are latency-bound.  Temporal blocking
-// (K steps per launch on shared-memory tiles) is opt-in (SW2D_TB=1): measured
-// slower than the per-step kernel on every paper size, kept
-// as a parity-tested experiment.
-constexpr long long kTbMaxCells = 1LL << 20;
-constexpr size_t kTbSmemMax = 200 * 1024;
-
-void plan_tb(sw2d* h, int sms) {
-  h->tb_k = 0;
-  const long long cells = h->p.nx * h->p.ny;
-  if (h->multi || h->virt || h->p.variant != SW2D_VARIANT_FUSED || h->red_level != 0) return;
-  if (cells > kTbMaxCells) return;
-  const char* on = std::getenv("SW2D_TB");
-  if (!on || std::atoi(on) == 0) return;
-  long long t = (long long)std::ceil(std::sqrt((double)cells / (double)sms));
-  t = std::max<long long>(8, std::min<long long>(t, 44));
-  int K = 8;
-  if (const char* e = std::getenv("SW2D_TB_K")) K = std::max(1, std::min(16, std::atoi(e)));
-  while (K > 1 && tb_smem_bytes((int)t, (int)t, K) > kTbSmemMax) --K;
-  if (K < 2) return;
-  h->tb_tw = h->tb_th = (int)t;
-  h->tb_k = K;
-}
-
-
 // Small grids: the persistent cooperative kernel (sw2d_persist.cu), on one
 // GPU without ranks, if its tiles fit co-resident.  By default where it
 // measured faster than the graph-replayed row march: up to
@@ -348,7 +322,7 @@ void plan_persist(sw2d* h) {
   const char* on = std::getenv("SW2D_PERSIST");
   if (on && std::atoi(on) == 0) return;
   if (!on) {   // the default: where it wins; a forced kernel kind (tests, A/B) wins too
-    if (std::getenv("SW2D_STEP_KERNEL") || h->tb_k) return;
+    if (std::getenv("SW2D_STEP_KERNEL")) return;
     if (cells > (h->red_level ? (1LL << 16) : (1LL << 18))) return;
   }
   int sms = 148;
@@ -476,21 +450,19 @@ void plan_launches(sw2d* h) {
     h->step_blocks2 = plan(h->launches2, per, std::max(1LL, (long long)sms * bps2 / ncc), mrows2, 2,
                            h->nstrips2);
   }
-  plan_tb(h, sms);
   plan_persist(h);
   {
-    static const char* kinds[] = {"warp-ring", "cta-ring", "small"};
+    static const char* kinds[] = {"", "cta-ring", "small"};
     std::string split = "grid";   // even-rows:<CTAs> if any two-step launch splits rows
     for (const Launch& L : h->launches2)
       if (L.sk > 0) split = "even-rows:" + std::to_string(L.sk);
     char buf[256];
     std::snprintf(buf, sizeof(buf),
                   "kernel=%s steps_per_launch=%d launches_per_pass=%zu strips=%d "
-                  "ctas_per_sm=%d halo=%s temporal_blocking=%d split=%s",
+                  "ctas_per_sm=%d halo=%s split=%s",
                   kinds[h->kind], h->launches2.empty() ? 1 : 2,
                   h->launches2.empty() ? h->launches.size() : h->launches2.size(), h->nstrips,
-                  bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", h->tb_k,
-                  split.c_str());
+                  bps, h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl", split.c_str());
     h->plan_text = buf;
     if (h->pk) {
       std::snprintf(buf, sizeof(buf),
@@ -502,9 +474,6 @@ void plan_launches(sw2d* h) {
     }
   }
   if (std::getenv("SW2D_VERBOSE")) {
-    if (h->tb_k)
-      std::fprintf(stderr, "[sw2d] temporal blocking: %dx%d tiles, %d steps per launch\n",
-                   h->tb_tw, h->tb_th, h->tb_k);
     std::fprintf(stderr, "[sw2d] kind %d red %d: %d CTAs/SM on %d SMs, %d strips\n", h->kind,
                  h->red_level, bps, sms, h->nstrips);
     for (const Launch& L : h->launches)
@@ -1052,7 +1021,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   if (h->halo_mode != SW2D_HALO_P2P && h->p.nx * h->p.ny <= kSmallMaxCells) h->kind = 2;
   if (const char* k = std::getenv("SW2D_STEP_KERNEL")) {
     const int v = std::atoi(k);
-    h->kind = (v == 0 || v == 2) ? v : 1;
+    h->kind = v == 2 ? 2 : 1;
   }
   if (h->halo_mode == SW2D_HALO_P2P) h->kind = 1;  // the fused halo lives in the CTA kernel
   if (const char* e = std::getenv("SW2D_FAULT_SKIP_HALO")) h->fault_skip_halo = std::atoll(e);
@@ -1510,36 +1479,6 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
         if (rc) return rc;
       }
       h->steps++;
-    }
-    return SW2D_OK;
-  }
-  if (h->tb_k) {  // temporally blocked: K steps per launch
-    Slab& sl = h->slabs[0];
-    int64_t left = nsteps;
-    while (left > 0) {
-      const int k = (int)std::min<int64_t>(left, h->tb_k);
-      TbArgs a;
-      a.E = sl.E[h->cur];
-      a.U = sl.U[h->cur];
-      a.V = sl.V[h->cur];
-      a.H0 = sl.H0;
-      a.En = sl.E[1 - h->cur];
-      a.Un = sl.U[1 - h->cur];
-      a.Vn = sl.V[1 - h->cur];
-      a.pitch = h->pitch;
-      a.jbase = sl.j0 + 1 - kHaloRows;
-      a.nx = (int)h->p.nx;
-      a.ny = (int)h->p.ny;
-      a.tw = h->tb_tw;
-      a.th = h->tb_th;
-      a.K = k;
-      a.c = h->coef;
-      launch_tb(a, h->stream);
-      h->nlaunch++;
-      CUDA_TRY(h, cudaGetLastError());
-      h->cur = 1 - h->cur;
-      h->steps += k;
-      left -= k;
     }
     return SW2D_OK;
   }

@@ -20,9 +20,6 @@ constexpr int kStripBase = kColOff - 3;  // storage column where strip 0's windo
 constexpr int kHaloRows = 4;         // halo rows per side: the cone of a two-step pass
 constexpr int kWarpsPerBlock = 4;      // grid-stride helper kernels
 constexpr int kThreads = 32 * kWarpsPerBlock;
-constexpr int kStepWarps = 1;          // step kernel: one warp per CTA (its strip
-                                       // and segment are CTA-uniform, so TMA
-                                       // operands live in uniform registers)
 constexpr int kOutLanes = 30;        // lanes 1..30 produce output; 0 and 31 are halo lanes
 constexpr int kColsPerStrip = 4 * kOutLanes;   // 120 output columns per warp strip
 
@@ -116,10 +113,9 @@ struct StepArgs {
 };
 
 // Step-kernel launchers (sw2d_kernels.cu).  `red_level`: 0 none, 1 sums
-// (VOLUME, SUM_ETA), 2 all diagnostics.  `kind`: 0 = one warp per CTA with
-// its own TMA row ring; 1 = CTA of kCtaStrips compute warps + a producer warp
-// sharing one TMA row ring (default); 2 = small grids: 2 columns per lane,
-// plain loads, 4 independent warps per CTA.
+// (VOLUME, SUM_ETA), 2 all diagnostics.  `kind`: 1 = CTA of kCtaStrips
+// compute warps + a producer warp sharing one TMA row ring (default); 2 =
+// small grids: 2 columns per lane, plain loads, 4 independent warps per CTA.
 int step_strips_per_cta(int kind);
 int step_strip_cols(int kind);   // output columns per warp strip (120, or 60 for kind 2)
 int step_grid(int kind, int nstrips, int nsegs);   // CTAs of one step launch
@@ -199,24 +195,6 @@ struct PaperArgs {
 void launch_paper_step(const PaperArgs& a, void* stream);   // 3 launches
 void launch_paper_init(const PaperArgs& a, void* stream);   // h, wet_out from H0 + E
 
-// Temporally blocked steps for small grids (sw2d_tb_kernels.cu): K steps per
-// launch on tw x th tiles with a 2K-cell apron in shared memory.
-struct TbArgs {
-  const float* E;
-  const float* U;
-  const float* V;
-  const float* H0;
-  float* En;
-  float* Un;
-  float* Vn;
-  long long pitch;
-  long long jbase;
-  int nx, ny;
-  int tw, th, K;
-  Coef c;
-};
-size_t tb_smem_bytes(int tw, int th, int K);
-void launch_tb(const TbArgs& a, void* stream);
 
 // Persistent cooperative kernel for small grids (sw2d_persist.cu): one launch
 // advances a whole grid `nsteps` steps; CTA t owns tile t (ntx x nty tiles of

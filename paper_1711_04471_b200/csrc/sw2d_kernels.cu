@@ -735,12 +735,7 @@ __device__ __forceinline__ void row_step(const Win& w, Win& o, const float4 E4, 
   row_stepC<RED, REMOTE, 4>(w, o, eL, h0L, uL, vL, L, x, acc, pU, pV, pE);
 }
 
-// --- TMA bulk-copy row ring (one per warp) ---------------------------------
-// Each warp streams its strip through a ring of kStages shared-memory stages;
-// a stage holds one row of the four input fields (4 x 512 B), filled by
-// cp.async.bulk (TMA) issued by lane 0 kStages-1 rows ahead and completed on
-// the stage's mbarrier (complete_tx).  The loads therefore need no registers
-// and several rows per warp are in flight.
+// --- TMA bulk copies and mbarriers (the CTA row rings below) ----------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -777,152 +772,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const float* src, uint32_
 
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-constexpr int kStages = 4;                        // rows in flight per warp
-constexpr int kRowBytes = 32 * 16;                // one field, one row, one strip
-constexpr int kStageBytes = 4 * kRowBytes;        // E, H0, U, V
-constexpr int kSmemPerWarp = kStages * kStageBytes;
-
-template <int RED>
-__global__ void __launch_bounds__(32 * kStepWarps)
-    sw2d_step_warp(const StepArgs a) {
-  constexpr bool REMOTE = false;
-  __shared__ __align__(128) unsigned char ring[kStepWarps][kSmemPerWarp];
-  __shared__ __align__(8) unsigned long long bars[kStepWarps][kStages];
-  const int lane = threadIdx.x & 31;
-  const int warp = kStepWarps == 1 ? 0 : (threadIdx.x >> 5);
-  const int gw = blockIdx.x * kStepWarps + warp;
-  const int strip = gw % a.nstrips;
-  const int seg = gw / a.nstrips;
-
-  Acc acc;
-  acc.init();
-
-  if (seg < a.nsegs) {  // warp-uniform
-    Ctx x;
-    x.ra = (int)a.row_lo + seg * a.rows_per_seg;
-    x.rb = min((int)a.row_hi, x.ra + a.rows_per_seg - 1);
-    const int c0 = strip * kColsPerStrip + kStripBase + lane * 4;  // storage column of element 0
-    const int k0 = c0 - kColOff;                      // its 1-based column
-    x.colmask = 0;
-    x.umask = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      x.colmask |= (k0 + c >= 1 && k0 + c <= a.nx) ? (1u << c) : 0u;
-      x.umask |= (k0 + c >= 1 && k0 + c <= a.nx - 1) ? (1u << c) : 0u;
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      x.cmf[c] = (x.colmask >> c) & 1u ? 1.0f : 0.0f;
-      x.umf[c] = (x.umask >> c) & 1u ? 1.0f : 0.0f;
-    }
-    x.cgx = a.c.cgx; x.cgy = a.c.cgy; x.cx = a.c.cx; x.cy = a.c.cy;
-    for (int c = 0; c < 4; ++c) x.cgxc[c] = x.umf[c] != 0.0f ? x.cgx : 0.0f;
-    for (int c = 0; c < 4; ++c) x.hminc[c] = x.cmf[c] != 0.0f ? a.c.hmin : __int_as_float(0x7f800000);
-    x.q = a.c.q; x.hmin = a.c.hmin; x.nz = a.c.nz;
-    x.ny = (int)a.ny;
-    x.out_lane = (lane >= 1) && (lane <= kOutLanes);
-#ifdef SW2D_DEBUG_BOUNDS
-    x.dU = a.s.Un;
-    x.dV = a.s.Vn;
-    x.dE = a.s.En;
-    x.nelem = a.s.nelem;
-#endif
-    const long long pitch = a.s.pitch;
-
-    const int first = x.ra - 2;      // first loaded row
-    const int last = x.rb + 2;       // last loaded row
-    // element offset of (row `first`, strip column 0) from each field's base
-    const long long off0 =
-        (long long)(first - (int)a.s.jbase) * pitch + strip * kColsPerStrip + kStripBase;
-    const uint32_t sbase = smem_u32(&ring[warp][0]);
-    const uint32_t bbase = smem_u32(&bars[warp][0]);
-
-    // lane 0: initialise the ring and issue rows first .. first+kStages-1
-    if (lane == 0) {
-#pragma unroll
-      for (int st = 0; st < kStages; ++st) mbar_init(bbase + 8 * st, 1);
-      fence_proxy_async();
-#pragma unroll
-      for (int st = 0; st < kStages; ++st) {
-        if (first + st <= last) {
-          const long long o = off0 + st * pitch;
-          SW2D_CHECK(o >= 0 && o + kRowBytes / 4 <= a.s.nelem);
-          const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
-          mbar_expect_tx(b, kStageBytes);
-          bulk_g2s(d, a.s.E + o, kRowBytes, b);
-          bulk_g2s(d + kRowBytes, a.s.H0 + o, kRowBytes, b);
-          bulk_g2s(d + 2 * kRowBytes, a.s.U + o, kRowBytes, b);
-          bulk_g2s(d + 3 * kRowBytes, a.s.V + o, kRowBytes, b);
-        }
-      }
-    }
-    __syncwarp();
-
-    Win wa, wb;
-    wa.zero();
-
-    float* __restrict__ En = a.s.En;
-    float* __restrict__ Un = a.s.Un;
-    float* __restrict__ Vn = a.s.Vn;
-    const long long lo = off0 + lane * 4;   // this lane's element offset, row `first`
-
-    // consume row `first + i` from stage i % kStages; refill it with row
-    // first + i + kStages
-    auto fetch = [&](int i, float4& E4, float4& H4, float4& U4, float4& V4) {
-      const int st = i & (kStages - 1);
-      const uint32_t b = bbase + 8 * st;
-      const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-      while (!mbar_try_wait(b, ph)) {
-      }
-      const float4* s4 = reinterpret_cast<const float4*>(&ring[warp][st * kStageBytes]) + lane;
-      E4 = s4[0];
-      H4 = s4[32];
-      U4 = s4[64];
-      V4 = s4[96];
-    };
-    auto refill = [&](int i) {
-      __syncwarp();
-      const int r = first + i + kStages;
-      if (lane == 0 && r <= last) {
-        const int st = i & (kStages - 1);
-        const long long o = off0 + (long long)(i + kStages) * pitch;
-        SW2D_CHECK(o >= 0 && o + kRowBytes / 4 <= a.s.nelem);
-        const uint32_t d = sbase + st * kStageBytes, b = bbase + 8 * st;
-        fence_proxy_async();
-        mbar_expect_tx(b, kStageBytes);
-        bulk_g2s(d, a.s.E + o, kRowBytes, b);
-        bulk_g2s(d + kRowBytes, a.s.H0 + o, kRowBytes, b);
-        bulk_g2s(d + 2 * kRowBytes, a.s.U + o, kRowBytes, b);
-        bulk_g2s(d + 3 * kRowBytes, a.s.V + o, kRowBytes, b);
-      }
-    };
-
-    const int n = last - first + 1;
-    int i = 0;
-    // two rows per trip: the window ping-pongs between wa and wb
-    for (; i + 1 < n; i += 2) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)i * pitch;
-      fetch(i, E4, H4, U4, V4);
-      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
-                    En + o - 2 * pitch);
-      refill(i);
-      fetch(i + 1, E4, H4, U4, V4);
-      row_step<RED, REMOTE>(wb, wa, E4, H4, U4, V4, first + i + 1, x, acc, Un + o + pitch, Vn + o,
-                    En + o - pitch);
-      refill(i + 1);
-    }
-    if (i < n) {
-      float4 E4, H4, U4, V4;
-      const long long o = lo + (long long)i * pitch;
-      fetch(i, E4, H4, U4, V4);
-      row_step<RED, REMOTE>(wa, wb, E4, H4, U4, V4, first + i, x, acc, Un + o, Vn + o - pitch,
-                    En + o - 2 * pitch);
-    }
-  }
-  if (RED >= 1) block_reduce_and_finalize<RED, kStepWarps>(acc, a.red);
 }
 
 // --- CTA-shared row ring with a producer warp (kind 1, the default) --------
@@ -1822,7 +1671,7 @@ int grid_stride_blocks(long long n) {
 
 #ifndef SW2D_PROBE   // tools/cta2_probe.cu: the kernels alone, one instantiation (SASS studies)
 int step_strips_per_cta(int kind) {
-  return kind == 1 ? kCtaStrips : (kind == 2 ? kSmallWarps : kStepWarps);
+  return kind == 2 ? kSmallWarps : kCtaStrips;
 }
 
 int step_strip_cols(int kind) { return kind == 2 ? kSmallCols : kColsPerStrip; }
@@ -1853,18 +1702,14 @@ void launch_kind(const StepArgs& a, int kind, cudaStream_t s) {
     sw2d_step_small<RED><<<blocks, 32 * kSmallWarps, 0, s>>>(a);
     return;
   }
-  if (kind == 1 || REMOTE) {
-    static unsigned long long attr_devices = 0;  // dynamic smem above 48 KB, per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(attr_devices >> (dev & 63) & 1ull)) {
-      cta_attributes<RED, REMOTE>();
-      attr_devices |= 1ull << (dev & 63);
-    }
-    sw2d_step_cta<RED, REMOTE><<<step_grid(1, a.nstrips, a.nsegs), kCtaThreads, kCtaSmem, s>>>(a);
-  } else {
-    sw2d_step_warp<RED><<<blocks, 32 * kStepWarps, 0, s>>>(a);
+  static unsigned long long attr_devices = 0;  // dynamic smem above 48 KB, per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_devices >> (dev & 63) & 1ull)) {
+    cta_attributes<RED, REMOTE>();
+    attr_devices |= 1ull << (dev & 63);
   }
+  sw2d_step_cta<RED, REMOTE><<<step_grid(1, a.nstrips, a.nsegs), kCtaThreads, kCtaSmem, s>>>(a);
 }
 
 template <int RED>
@@ -1872,12 +1717,10 @@ int occupancy_kind(int kind) {
   int n = 0;
   if (kind == 2) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_small<RED>, 32 * kSmallWarps, 0);
-  } else if (kind == 1) {
+  } else {
     cta_attributes<RED, false>();
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_cta<RED, false>, kCtaThreads,
                                                   kCtaSmem);
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sw2d_step_warp<RED>, 32 * kStepWarps, 0);
   }
   return n < 1 ? 1 : n;
 }
