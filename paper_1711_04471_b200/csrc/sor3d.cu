@@ -77,6 +77,7 @@ struct Args {
   long long pitch, plane;  // elements
   int nx, ny, nz, kz;
   float cx, cy, cz, dd, invd, om, om1;
+  float negz;  // -0.0f: the packed products' addend (a parameter: opaque to ptxas)
   Red red;
 };
 
@@ -214,11 +215,21 @@ struct March {
   float amx;
 };
 
+// Storage slot of cell c (0..3) of an aligned x-quad: the packed layout
+// (SOR_PACKED, below) keeps a quad (c0, c1, c2, c3) as (c0, c2, c1, c3).
+#ifndef SOR_PACKED
+#define SOR_PACKED 1
+#endif
+__host__ __device__ constexpr int slot(int c) {
+  return SOR_PACKED ? (c == 1 ? 2 : (c == 2 ? 1 : c)) : c;
+}
 __device__ __forceinline__ float& comp(float4& v, int c) {
-  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+  const int k = slot(c);
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 __device__ __forceinline__ float compv(const float4& v, int c) {
-  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+  const int k = slot(c);
+  return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w));
 }
 
 struct Lane {
@@ -294,7 +305,7 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
         } else if (L.outm) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (L.outm >> c & 1) st.op[c] = compv(o, c);
+            if (L.outm >> c & 1) st.op[slot(c)] = compv(o, c);
         }
       } else {
         float* op = a.pout + (st.ofs - 4u * (unsigned)L.plane);
@@ -303,7 +314,7 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
         } else if (L.anyout) {
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (L.outm >> c & 1) op[c] = compv(o, c);
+            if (L.outm >> c & 1) op[slot(c)] = compv(o, c);
         }
       }
     }
@@ -328,15 +339,170 @@ __device__ __forceinline__ void step(March& st, const Lane& L, const Args& a, in
   }
 }
 
+// --- packed form (SOR_PACKED): the storage keeps each aligned x-quad of
+// cells (c0, c1, c2, c3) as (c0, c2, c1, c3), so a lane's float4 holds the
+// pair of one colour in .x/.y (c0, c2) and the other in .z/.w (c1, c3): the
+// two cells of one colour in a step are one register pair and every
+// operation of their update is one paired instruction (FADD2, and FFMA2
+// with a -0 addend for the products, rounding like mul.rn: the 2DSW
+// kernel's R25).  Same operations per cell, same order: bitwise.
+struct f2 {
+  float a, b;
+};
+__device__ __forceinline__ f2 add2(f2 x, f2 y) {
+  f2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(r.a), "=f"(r.b) : "f"(x.a), "f"(x.b), "f"(y.a), "f"(y.b));
+  return r;
+}
+__device__ __forceinline__ f2 sub2(f2 x, f2 y) {
+  f2 r;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(r.a), "=f"(r.b) : "f"(x.a), "f"(x.b), "f"(y.a), "f"(y.b));
+  return r;
+}
+// c * x (c broadcast) rounded once: fma(c, x, -0)
+__device__ __forceinline__ f2 mul2(float c, f2 x, float nz) {
+  f2 r;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%2};\n\tmov.b64 rb, {%3,%4};\n\t"
+      "mov.b64 rc, {%5,%5};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(r.a), "=f"(r.b) : "f"(c), "f"(x.a), "f"(x.b), "f"(nz));
+  return r;
+}
+// nsum = (cx (E + W) + cy (N + S)) + cz (U + D), per element as nsum()
+__device__ __forceinline__ f2 nsum2(f2 e, f2 w, f2 n, f2 s, f2 u, f2 d, const Args& a) {
+  return add2(add2(mul2(a.cx, add2(e, w), a.negz), mul2(a.cy, add2(n, s), a.negz)),
+              mul2(a.cz, add2(u, d), a.negz));
+}
+// om1 p + om ((nsum - rhs) invd), per element as upd()
+__device__ __forceinline__ f2 upd2(f2 p, f2 ns, f2 rh, const Args& a) {
+  return add2(mul2(a.om1, p, a.negz), mul2(a.om, mul2(a.invd, sub2(ns, rh), a.negz), a.negz));
+}
+__device__ __forceinline__ f2 lo(const float4& v) { return f2{v.x, v.y}; }   // cells 0, 2
+__device__ __forceinline__ f2 hi(const float4& v) { return f2{v.z, v.w}; }   // cells 1, 3
+template <int P>
+__device__ __forceinline__ f2 cls(const float4& v) { return P ? hi(v) : lo(v); }
+template <int P>
+__device__ __forceinline__ void set_cls(float4& v, f2 x) {
+  if (P) { v.z = x.a; v.w = x.b; } else { v.x = x.a; v.y = x.b; }
+}
+// x neighbours of the colour-P pair of quad q (cells P, P+2): W, E pairs.
+// prev_w: the previous lane's cell 3 (.w), next_x: the next lane's cell 0 (.x)
+template <int P>
+__device__ __forceinline__ void xnb(const float4& q, float prev_w, float next_x, f2& w, f2& e) {
+  if (P == 0) {   // cells 0, 2: W = (c-1, c1), E = (c1, c3)
+    w = f2{prev_w, q.z};
+    e = hi(q);
+  } else {        // cells 1, 3: W = (c0, c2), E = (c2, c4)
+    w = lo(q);
+    e = f2{q.y, next_x};
+  }
+}
+
+// One march step in the packed form (see step()): the same schedule, the
+// updated class of the step is the register pair cls<P>.
+template <int R, int P, int S, bool RES, bool WRITE, bool H>
+__device__ __forceinline__ void step_packed(March& st, const Lane& L, const Args& a, int m,
+                                            float4 (*s_in)[R][kSx], float4 (*s_new)[R][kSx]) {
+  const int tx = L.tx, ty = L.ty;
+  s_in[S][ty][tx] = st.pz1;
+  __syncthreads();
+  const float4 N = lds4(&s_in[S][L.yn][tx]), S4 = lds4(&s_in[S][L.ys][tx]);
+  const float pw = __shfl_up_sync(kFull, st.pz1.w, 1, kSx);
+  const float nxv = __shfl_down_sync(kFull, st.pz1.x, 1, kSx);
+  float4 pn = st.pz1;
+  const bool mint = m >= 1 && m <= L.nz;
+  {
+    f2 w, e;
+    xnb<P>(st.pz1, pw, nxv, w, e);
+    const f2 ns = nsum2(e, w, cls<P>(N), cls<P>(S4), cls<P>(st.pz2), cls<P>(st.pz0), a);
+    const f2 nv = upd2(cls<P>(st.pz1), ns, cls<P>(st.r2), a);
+    // red update of interior cells (apron cells outside the box are never read)
+    const f2 old = cls<P>(st.pz1);
+    const int b0 = L.intr >> P & 1, b1 = L.intr >> (P + 2) & 1;
+    set_cls<P>(pn, f2{(mint && b0) ? nv.a : old.a, (mint && b1) ? nv.b : old.b});
+    if (RES && m >= L.k0 && m <= L.k1) {
+      // residual r = rhs - (nsum - dd p) of all four cells: this class, then the other
+      const f2 r1 = sub2(cls<P>(st.r2), sub2(ns, mul2(a.dd, cls<P>(st.pz1), a.negz)));
+      f2 w2, e2;
+      xnb<P ^ 1>(st.pz1, pw, nxv, w2, e2);
+      const f2 ns2 = nsum2(e2, w2, cls<P ^ 1>(N), cls<P ^ 1>(S4), cls<P ^ 1>(st.pz2),
+                           cls<P ^ 1>(st.pz0), a);
+      const f2 r2 = sub2(cls<P ^ 1>(st.r2), sub2(ns2, mul2(a.dd, cls<P ^ 1>(st.pz1), a.negz)));
+      const float rr[4] = {r1.a, r1.b, r2.a, r2.b};
+      const int cc[4] = {P, P + 2, P ^ 1, (P ^ 1) + 2};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (L.outm >> cc[t] & 1) {
+          st.acc = fma((double)rr[t], (double)rr[t], st.acc);
+          st.amx = fmaxf(st.amx, fabsf(rr[t]));
+        }
+    }
+  }
+  if (WRITE) {
+    s_new[S][ty][tx] = pn;  // read by the black phase of step m+1
+    const float4 Nb = lds4(&s_new[S ^ 1][L.yn][tx]), Sb = lds4(&s_new[S ^ 1][L.ys][tx]);
+    const float pwb = __shfl_up_sync(kFull, st.n1.w, 1, kSx);
+    const float nxb = __shfl_down_sync(kFull, st.n1.x, 1, kSx);
+    if (m - 1 >= L.k0 && m - 1 <= L.k1) {
+      // black cells of plane m-1 (computed everywhere, stored on output cells)
+      float4 o = st.n1;
+      f2 w, e;
+      xnb<P>(st.n1, pwb, nxb, w, e);
+      const f2 ns = nsum2(e, w, cls<P>(Nb), cls<P>(Sb), cls<P>(pn), cls<P>(st.n0), a);
+      set_cls<P>(o, upd2(cls<P>(st.n1), ns, cls<P>(st.r1), a));
+      float* op = RES ? st.op : a.pout + (st.ofs - 4u * (unsigned)L.plane);
+      if (L.all4) {
+        sth<H>(op, o);
+      } else if (L.anyout) {
+        // storage slot k of the quad holds cell (0, 2, 1, 3)[k]
+        if (L.outm & 1) op[0] = o.x;
+        if (L.outm & 4) op[1] = o.y;
+        if (L.outm & 2) op[2] = o.z;
+        if (L.outm & 8) op[3] = o.w;
+      }
+    }
+  }
+  st.pz0 = st.pz1;
+  st.pz1 = st.pz2;
+  st.pz2 = st.pf;
+  st.pf = ldh<H, false>(RES ? st.pp : a.pin + st.ofs);
+  st.r1 = st.r2;
+  st.r2 = st.rf1;
+  st.rf1 = st.rf2;
+  st.rf2 = ldh<H, true>(RES ? st.rp : a.rhs + st.ofs);
+  st.n0 = st.n1;
+  st.n1 = pn;
+  if constexpr (RES) {
+    st.pp += L.plane;
+    st.rp += L.plane;
+    st.op += L.plane;
+  } else {
+    st.ofs += (unsigned)L.plane;
+  }
+}
+
 template <int R, int P0, bool RES, bool WRITE, bool H>
 __device__ __forceinline__ void march(March& st, const Lane& L, const Args& a, int nsteps,
                                       float4 (*s_in)[R][kSx], float4 (*s_new)[R][kSx]) {
   for (int s = 0; s < nsteps; s += 4) {
     const int m = L.m0 + s;
-    step<R, P0, 0, RES, WRITE, H>(st, L, a, m, s_in, s_new);
-    step<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 1, s_in, s_new);
-    step<R, P0, 0, RES, WRITE, H>(st, L, a, m + 2, s_in, s_new);
-    step<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 3, s_in, s_new);
+    // the packed step where it measured faster: without the residual (its
+    // extra registers spill the residual variants at 64 per thread), on
+    // L2-resident grids (H; sor300 2.46e11 -> 2.78e11, sor1024 slower)
+    if constexpr (SOR_PACKED && !RES && H) {
+      step_packed<R, P0, 0, RES, WRITE, H>(st, L, a, m, s_in, s_new);
+      step_packed<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 1, s_in, s_new);
+      step_packed<R, P0, 0, RES, WRITE, H>(st, L, a, m + 2, s_in, s_new);
+      step_packed<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 3, s_in, s_new);
+    } else {
+      step<R, P0, 0, RES, WRITE, H>(st, L, a, m, s_in, s_new);
+      step<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 1, s_in, s_new);
+      step<R, P0, 0, RES, WRITE, H>(st, L, a, m + 2, s_in, s_new);
+      step<R, P0 ^ 1, 1, RES, WRITE, H>(st, L, a, m + 3, s_in, s_new);
+    }
   }
 }
 
@@ -497,6 +663,7 @@ Args make_args(const sor3d* h) {
   a.invd = h->invd;
   a.om = h->om;
   a.om1 = h->om1;
+  a.negz = -0.0f;
   a.red.part = h->part;
   a.red.counter = h->counter;
   a.red.rec = nullptr;
@@ -541,6 +708,17 @@ double* next_record(sor3d* h) {
   return r;
 }
 
+// storage index of a cell at padded position x (rows and planes are whole
+// quads): the packed layout keeps quad (c0, c1, c2, c3) as (c0, c2, c1, c3)
+__device__ __forceinline__ long long store_slot(long long x) {
+#if SOR_PACKED
+  const int q = (int)(x & 3);
+  return (x & ~3LL) | (q == 1 ? 2 : (q == 2 ? 1 : q));
+#else
+  return x;
+#endif
+}
+
 // Dense [nz][ny][nx] <-> padded storage, one grid-stride pass: TO_PAD also
 // counts non-finite values (sor3d_set's check).
 template <bool TO_PAD>
@@ -552,12 +730,13 @@ __global__ void repack(float* pad, const float* din, float* dout, int nx, int ny
     const long long po = (k + 1 + kPlaneOff) * plane + (j + 1 + kRowOff) * pitch + 1 + kColOff;
     const long long dofs = row * nx;
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      const long long q = store_slot(po + i);
       if (TO_PAD) {
         const float v = din[dofs + i];
         nb += !isfinite(v);
-        pad[po + i] = v;
+        pad[q] = v;
       } else {
-        dout[dofs + i] = pad[po + i];
+        dout[dofs + i] = pad[q];
       }
     }
   }

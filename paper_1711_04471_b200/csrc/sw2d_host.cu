@@ -73,7 +73,7 @@ struct sw2d {
   int kind = 1;  // step kernel kind (sw2d_internal.cuh); SW2D_STEP_KERNEL overrides
   // persistent cooperative kernel (small grids): K steps per shared-memory
   // block, pntx x pnty tiles of pth rows, one CTA each; pk = 0: off
-  int pk = 0, pth = 0, pntx = 0, pnty = 0;
+  int pk = 0, pshape = 0, pth = 0, pntx = 0, pnty = 0;
   unsigned* pflags = nullptr;   // per-tile step counters
   unsigned pbase = 0;           // their value before the next launch
   RedPartial* ppart = nullptr;  // per-step CTA partials of one launch chunk
@@ -104,8 +104,11 @@ struct sw2d {
   double* h0sum = nullptr;  // sum of hzero over the cells this handle owns
   double* zero = nullptr;   // a device 0.0
   int* bad = nullptr;
+  int* bad_host = nullptr;   // mapped pinned host word: set_state's verdict without a DMA
   unsigned char* wetbuf = nullptr;
   size_t wetbuf_bytes = 0;
+  float* stage = nullptr;   // dense [field][rows][nx] staging of host transfers (1D DMA)
+  size_t stage_floats = 0;
   float* snap[2] = {nullptr, nullptr};   // periodic-output staging buffers
   size_t snap_bytes = 0;
   cudaStream_t copy = nullptr;
@@ -307,12 +310,11 @@ float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch;
 // Small grids: the persistent cooperative kernel (sw2d_persist.cu), on one
 // GPU without ranks, if its tiles fit co-resident.  By default where it
 // measured faster than the graph-replayed row march: up to
-// 2^18 cells without per-step diagnostics (C1 1.55 vs 2.65 us/step, C2 3.58
-// vs 3.68), up to 2^16 with them; SW2D_PERSIST=0/1 forces it off/on (on: up
-// to 2^21 cells).  K = 2 steps per block (SW2D_PERSIST_K); tile rows
-// th = 16 rw - 4K with rw (rows per thread, 1..3; SW2D_PERSIST_RW) chosen to
-// minimise rw x (ceil(tiles / SMs) + 1) / 2 — a second CTA on an SM overlaps
-// the first one's latency (measured: C2 rw 2 on 189 tiles beats rw 3 on 117).
+// 2^18 cells (C1 1.55 vs 2.49 us/step, C2 3.25 vs 3.62; with VOLUME per step
+// 1.96 vs 2.92 and 3.54 vs 3.94); SW2D_PERSIST=0/1 forces it off/on (on: up
+// to 2^21 cells).  K = 2 steps per block (SW2D_PERSIST_K); the CTA shape
+// (warps x rows per thread; SW2D_PERSIST_SHAPE) minimises the busiest SM's
+// work, see below.
 constexpr int kPersistRedChunk = 64;   // steps per launch when diagnostics are folded
 void plan_persist(sw2d* h) {
   h->pk = 0;
@@ -323,27 +325,34 @@ void plan_persist(sw2d* h) {
   if (on && std::atoi(on) == 0) return;
   if (!on) {   // the default: where it wins; a forced kernel kind (tests, A/B) wins too
     if (std::getenv("SW2D_STEP_KERNEL")) return;
-    if (cells > (h->red_level ? (1LL << 16) : (1LL << 18))) return;
+    if (cells > (1LL << 18)) return;
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
   int K = 2;
   if (const char* e = std::getenv("SW2D_PERSIST_K")) K = std::atoi(e) == 1 ? 1 : 2;
-  int rw_force = 0;
-  if (const char* e = std::getenv("SW2D_PERSIST_RW")) rw_force = std::max(1, std::min(3, std::atoi(e)));
+  int shape_force = -1;
+  if (const char* e = std::getenv("SW2D_PERSIST_SHAPE"))
+    shape_force = std::max(0, std::min(persist_shapes() - 1, std::atoi(e)));
   const int tw = persist_tile_cols(K);
   const int ntx = (int)((h->p.nx + tw - 1) / tw);
-  long long best = -1;
-  for (int rw = 1; rw <= 3; ++rw) {
-    if (rw_force && rw != rw_force) continue;
-    const int th = persist_tile_rows(K, rw);
+  // the shape that minimises the busiest SM's work (ties: the first, more warps)
+  double best = -1;
+  for (int sh = 0; sh < persist_shapes(); ++sh) {
+    if (shape_force >= 0 && sh != shape_force) continue;
+    const int th = persist_tile_rows(K, sh);
     const int nty = (int)((h->p.ny + th - 1) / th);
     const long long nt = (long long)ntx * nty;
-    if (nt > persist_capacity(K, h->red_level, rw)) continue;
-    const long long cost = rw * ((nt + sms - 1) / sms + 1);
-    if (best < 0 || cost < best) {
+    if (nt > persist_capacity(K, h->red_level, sh)) continue;
+    // the busiest SM's shared rows; a lone CTA per SM counted 1.5x (nothing
+    // overlaps its handshake).  Measured on C2: 8 warps x 24 rows, 288 tiles
+    // (2 per SM) 3.18 us/step; 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
+    const long long per_sm = (nt + sms - 1) / sms;
+    const double cost = (double)persist_shape_rows(sh) * (per_sm == 1 ? 1.5 : (double)per_sm);
+    if (best < 0 || cost < best - 1e-9) {
       best = cost;
       h->pk = K;
+      h->pshape = sh;
       h->pth = th;
       h->pntx = ntx;
       h->pnty = nty;
@@ -466,9 +475,10 @@ void plan_launches(sw2d* h) {
     h->plan_text = buf;
     if (h->pk) {
       std::snprintf(buf, sizeof(buf),
-                    "kernel=persist steps_per_block=%d tiles=%dx%d tile=%dx%d cooperative=1 "
-                    "halo=%s",
+                    "kernel=persist steps_per_block=%d tiles=%dx%d tile=%dx%d warps=%d "
+                    "cooperative=1 halo=%s",
                     h->pk, h->pntx, h->pnty, persist_tile_cols(h->pk), h->pth,
+                    persist_shape_warps(h->pshape),
                     h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl");
       h->plan_text = buf;
     }
@@ -788,7 +798,9 @@ void free_all(sw2d* h) {
   cudaFree(h->h0sum);
   cudaFree(h->zero);
   cudaFree(h->bad);
+  if (h->bad_host) cudaFreeHost(h->bad_host);
   cudaFree(h->wetbuf);
+  cudaFree(h->stage);
   cudaFree(h->snap[0]);
   cudaFree(h->snap[1]);
   for (int b = 0; b < 2; ++b) {
@@ -1071,7 +1083,8 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     const size_t fw = persist_flag_words((int)nt);
     CUDA_TRY(h, cudaMalloc(&h->pflags, fw * sizeof(unsigned)));
     CUDA_TRY(h, cudaMemsetAsync(h->pflags, 0, fw * sizeof(unsigned), h->stream));
-    CUDA_TRY(h, cudaMalloc(&h->ppart, nt * kPersistRedChunk * sizeof(RedPartial)));
+    CUDA_TRY(h, cudaMalloc(&h->ppart, nt * (size_t)persist_shape_warps(h->pshape) *
+                                          kPersistRedChunk * sizeof(RedPartial)));
   }
   // reduction scratch
   long long cap = std::max<long long>(h->step_blocks, 2LL * h->step_blocks2);
@@ -1101,6 +1114,7 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
   CUDA_TRY(h, cudaMemsetAsync(h->zero, 0, sizeof(double), h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->h0sum, 0, sizeof(double), h->stream));
   CUDA_TRY(h, cudaMalloc(&h->bad, sizeof(int)));
+  CUDA_TRY(h, cudaHostAlloc(&h->bad_host, sizeof(int), cudaHostAllocMapped));
   // real ranks: the sync buffer (flags, record slots), then the NCCL
   // communicator (SW2D_BOOT_NCCL), which in P2P mode only all-gathers the blobs
   if (h->multi) {
@@ -1145,6 +1159,54 @@ __global__ void ring_scatter(const double* grec, double* hist, int len,
   }
   __syncthreads();
   if (threadIdx.x == 0) *dstep = s0 + (unsigned long long)n;
+}
+
+__global__ void publish_word(const int* src, int* dst_host_mapped) {
+  *(volatile int*)dst_host_mapped = *src;
+}
+
+// 2D copy between a dense [rows][nx] array and the pitched field layout (the
+// device side of host transfers: the host side is one contiguous DMA per
+// field, which runs at full PCIe rate in both directions at once — pitched
+// cudaMemcpy2DAsync transfers did not overlap with each other)
+__global__ void copy_rows(float* dst, long long dpitch, const float* src, long long spitch,
+                          long long nrows, int nx) {
+  const long long n = nrows * (long long)nx;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / nx, c = i - r * nx;
+    dst[r * dpitch + c] = src[r * spitch + c];
+  }
+}
+
+void launch_copy_rows(sw2d* h, float* dst, long long dpitch, const float* src, long long spitch,
+                      long long nrows) {
+  const long long n = nrows * h->p.nx;
+  if (n <= 0) return;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+  copy_rows<<<blocks, 256, 0, h->stream>>>(dst, dpitch, src, spitch, nrows, (int)h->p.nx);
+  h->nlaunch++;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// dense staging for `fields` fields of the handle's rows
+int ensure_stage(sw2d* h, int fields, int64_t rows) {
+  const size_t need = (size_t)fields * (size_t)rows * (size_t)h->p.nx;
+  if (need <= h->stage_floats) return SW2D_OK;
+  cudaFree(h->stage);
+  h->stage = nullptr;
+  h->stage_floats = 0;
+  CUDA_TRY(h, cudaMalloc(&h->stage, need * sizeof(float)));
+  h->stage_floats = need;
+  return SW2D_OK;
 }
 
 int run_pass(sw2d* h, int spl) {
@@ -1376,21 +1438,39 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
   const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
   const size_t wbytes = (size_t)nx * sizeof(float);
   const size_t dp = (size_t)h->pitch * sizeof(float);
+  int64_t rows = 0;
+  for (Slab& s : h->slabs) rows += s.nrows;
+  const size_t cells = (size_t)rows * (size_t)nx;
   CUDA_TRY(h, cudaMemsetAsync(h->bad, 0, sizeof(int), h->stream));
+  const float* src[4] = {hzero, eta, u, v};
+  // host arrays: one contiguous DMA per field into the dense stage, then a
+  // device copy into the pitched fields; device arrays: the device copy alone
+  const float* dense[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int f = 0; f < 4; ++f) {
+    if (!src[f]) continue;
+    if (is_device_ptr(src[f])) {
+      dense[f] = src[f];
+      continue;
+    }
+    int rc = ensure_stage(h, 4, rows);
+    if (rc) return rc;
+    float* st = h->stage + (size_t)f * cells;
+    CUDA_TRY(h, cudaMemcpyAsync(st, src[f], cells * sizeof(float), cudaMemcpyHostToDevice,
+                                h->stream));
+    dense[f] = st;
+  }
   for (Slab& s : h->slabs) {
     const size_t src_off = (size_t)(s.j0 - hj0) * (size_t)nx;
     float* dst[4] = {s.H0, s.E[0], s.U[0], s.V[0]};
-    const float* src[4] = {hzero, eta, u, v};
     for (int f = 0; f < 4; ++f) {
       float* d = dst[f] + kHaloRows * h->pitch + 1 + kColOff;
-      if (src[f]) {
-        CUDA_TRY(h, cudaMemcpy2DAsync(d, dp, src[f] + src_off, wbytes, wbytes,
-                                      (size_t)s.nrows, cudaMemcpyDefault, h->stream));
-      } else {
+      if (dense[f])
+        launch_copy_rows(h, d, h->pitch, dense[f] + src_off, nx, s.nrows);
+      else
         CUDA_TRY(h, cudaMemset2DAsync(d, dp, 0, wbytes, (size_t)s.nrows, h->stream));
-      }
     }
   }
+  CUDA_TRY(h, cudaGetLastError());
   // finiteness, wall faces, sum(hzero) — one fold over all slabs
   int expected = 0;
   std::vector<IngestArgs> ias;
@@ -1449,8 +1529,14 @@ int sw2d_set_state(sw2d* h, const float* hzero, const float* eta,
     CUDA_TRY(h, cudaGetLastError());
   }
   int bad = 0;
-  CUDA_TRY(h, cudaMemcpyAsync(&bad, h->bad, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  // the verdict reaches the host by a kernel store into mapped host memory,
+  // not a copy: a device-to-host DMA would queue behind another handle's
+  // multi-GB download on the same copy engine (the e2e pipeline, §8)
+  publish_word<<<1, 1, 0, h->stream>>>(h->bad, h->bad_host);
+  h->nlaunch++;
+  CUDA_TRY(h, cudaGetLastError());
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  bad = *(volatile int*)h->bad_host;
   h->cur = 0;
   h->steps = 0;
   h->pending.clear();
@@ -1498,6 +1584,7 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       a.jbase = sl.j0 + 1 - kHaloRows;
       a.nx = (int)h->p.nx;
       a.ny = (int)h->p.ny;
+      a.shape = h->pshape;
       a.th = h->pth;
       a.ntx = h->pntx;
       a.nty = h->pnty;
@@ -1516,7 +1603,8 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
                                             cudaGetErrorString((cudaError_t)e));
       h->nlaunch++;
       if (h->red_level) {
-        launch_fold_steps(h->ppart, h->pntx * h->pnty, (int)chunk, h->hist, h->hist_len,
+        launch_fold_steps(h->ppart, h->pntx * h->pnty * persist_shape_warps(h->pshape),
+                          (int)chunk, h->hist, h->hist_len,
                           h->dstep, h->h0sum, (double)h->p.dx * (double)h->p.dy, h->stream);
         h->nlaunch++;
       }
@@ -1724,8 +1812,6 @@ int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
   ENTER(h);
   if (!h->state_set) return fail(h, SW2D_ESTATE, "sw2d_get_state before sw2d_set_state");
   const int64_t nx = h->p.nx, hj0 = h->slabs.front().j0;
-  const size_t wbytes = (size_t)nx * sizeof(float);
-  const size_t dp = (size_t)h->pitch * sizeof(float);
   int64_t total_rows = 0;
   for (Slab& s : h->slabs) total_rows += s.nrows;
   if (wet) {
@@ -1738,16 +1824,28 @@ int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
       h->wetbuf_bytes = need;
     }
   }
+  // device arrays: a device copy out of the pitched fields; host arrays: the
+  // same into the dense stage, then one contiguous DMA per field
+  float* outp[3] = {eta, u, v};
+  float* dense[3] = {nullptr, nullptr, nullptr};
+  const size_t cells = (size_t)total_rows * (size_t)nx;
+  for (int f = 0; f < 3; ++f) {
+    if (!outp[f]) continue;
+    if (is_device_ptr(outp[f])) {
+      dense[f] = outp[f];
+      continue;
+    }
+    int rc = ensure_stage(h, 4, total_rows);
+    if (rc) return rc;
+    dense[f] = h->stage + (size_t)f * cells;
+  }
   for (Slab& s : h->slabs) {
     const size_t off = (size_t)(s.j0 - hj0) * (size_t)nx;
-    float* dst[3] = {eta, u, v};
     const float* src[3] = {s.E[h->cur], s.U[h->cur], s.V[h->cur]};
-    for (int f = 0; f < 3; ++f) {
-      if (!dst[f]) continue;
-      CUDA_TRY(h, cudaMemcpy2DAsync(dst[f] + off, wbytes,
-                                    src[f] + kHaloRows * h->pitch + 1 + kColOff, dp,
-                                    wbytes, (size_t)s.nrows, cudaMemcpyDefault, h->stream));
-    }
+    for (int f = 0; f < 3; ++f)
+      if (dense[f])
+        launch_copy_rows(h, dense[f] + off, nx, src[f] + kHaloRows * h->pitch + 1 + kColOff,
+                         h->pitch, s.nrows);
     if (wet) {
       launch_wet(s.E[h->cur], s.H0, h->pitch, s.nrows, (int)nx, h->p.hmin,
                  h->wetbuf + off, h->stream);
@@ -1755,6 +1853,10 @@ int sw2d_get_state(sw2d* h, float* eta, float* u, float* v, uint8_t* wet) {
     }
   }
   CUDA_TRY(h, cudaGetLastError());
+  for (int f = 0; f < 3; ++f)
+    if (dense[f] && dense[f] != outp[f])
+      CUDA_TRY(h, cudaMemcpyAsync(outp[f], dense[f], cells * sizeof(float),
+                                  cudaMemcpyDeviceToHost, h->stream));
   if (wet)
     CUDA_TRY(h, cudaMemcpyAsync(wet, h->wetbuf, (size_t)total_rows * (size_t)nx,
                                 cudaMemcpyDefault, h->stream));

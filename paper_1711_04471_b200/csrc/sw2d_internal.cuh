@@ -208,7 +208,8 @@ struct PersistArgs {
   long long pitch;
   long long jbase;           // global 1-based row of storage row 0
   int nx, ny;
-  int th;                    // tile rows (16 rw - 4K)
+  int shape;                 // CTA shape (persist_shape_*)
+  int th;                    // tile rows (persist_tile_rows)
   int ntx, nty;              // tiles across / down
   int cur;                   // buffer holding the state at the first step
   int nsteps;
@@ -217,10 +218,14 @@ struct PersistArgs {
   Coef c;
   RedPartial* part;          // [nsteps][ntiles] per-step CTA partials (RED >= 1)
 };
+// CTA shapes (0 .. persist_shapes()-1): warps per CTA x shared rows per thread
+int persist_shapes();
+int persist_shape_rows(int shape);       // shared-tile rows
+int persist_shape_warps(int shape);
 int persist_tile_cols(int K);
-int persist_tile_rows(int K, int rw);    // rw: tile rows per thread (1..3)
+int persist_tile_rows(int K, int shape);
 size_t persist_flag_words(int ntiles);   // flag array length (one 128-byte line per tile)
-int persist_capacity(int K, int red_level, int rw);   // co-resident CTAs
+int persist_capacity(int K, int red_level, int shape);   // co-resident CTAs
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream);  // 0 or cudaError
 
 // wet mask of the current state into a dense uint8 [nrows][nx] buffer.

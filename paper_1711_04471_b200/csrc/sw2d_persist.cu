@@ -5,28 +5,34 @@
 // in L2 and one step is a few microseconds of work spread over the GPU, so a
 // kernel launch (or graph node) per pass and the start-up of a row march
 // cost more than the arithmetic.  Here ONE cooperative launch runs many
-// steps: every CTA owns a fixed tile of TW x TH cells (TW = 64 - 2A, A = 2K)
-// for the whole launch and advances it K steps at a time in shared memory
-// (tile + A-cell apron: the dependency cone of K steps is 2K cells), then
-//   * stores the tile's exact centre into the next state buffer (L2),
-//   * publishes a per-tile step counter (release),
+// steps: every CTA owns a fixed tile of (64 - 4K) x (PW RW - 4K) cells for
+// the whole launch and advances it K steps at a time in shared memory (tile
+// + 2K-cell apron: the dependency cone of K steps), then
+//   * stores the outer ring of the tile's exact centre (all of it after the
+//     last block) into the next state buffer (L2),
+//   * publishes a per-tile step counter (st.release.gpu, own 128-byte line),
 //   * waits until its 8 neighbour tiles have published the same block
-//     (acquire) — they have then written the apron it needs and finished
-//     reading the buffer it will overwrite next (double buffering),
+//     (ld.acquire.gpu, back-off) — they have then written the apron it needs
+//     and finished reading the buffer it will overwrite next,
 //   * reloads only its apron ring; the centre stays in shared memory.
 // There is no grid-wide barrier and no relaunch.  The blocks wait on one
 // another, so the launch is cooperative (all CTAs co-resident, guaranteed by
 // the driver) — the one sanctioned form of inter-CTA waiting on one GPU.
 //
-// Per step and cell the arithmetic is the oracle's, operation for operation,
-// in four CTA-synchronised phases (h and wet; face velocities; etan; Shapiro
-// + commit), like the oracle's loop nests (oracle/sw2d_ref.c): bitwise parity.
-// Cells outside the grid are dry with zero velocity (the closed basin).  The
-// apron's outer cells go stale one ring per phase and never reach the centre.
+// A step is three phases separated by CTA barriers: (h, wet, u', v'),
+// (etan), (Shapiro filter + commit).  Each thread keeps its 2 x RW cells in
+// registers across the phases; x neighbours come from warp shuffles (a warp
+// owns a 64-column shared row, 2 columns per lane), y neighbours through
+// shared memory.  Every operation is the oracle's, in its order
+// (oracle/sw2d_ref.c; the face rule and the exact flag FMAs as in the row
+// march, R24): bitwise parity.  Cells outside the grid are dry with zero
+// velocity (the closed basin); the apron's outer cells go stale two rings
+// per step and never reach the centre.
 //
-// Diagnostics: per step, each CTA folds its centre cells (fp64 sums, exact
-// max/min/count) into one partial; fold_steps folds the partials of a launch
-// in a fixed order after it (deterministic; the deferred fold of the graphs).
+// Diagnostics: per step, each warp folds its centre cells (fp64 sums, exact
+// max/min/count) into one partial — no CTA barrier for it; fold_steps folds
+// the partials of a launch in a fixed order after it (deterministic; the
+// deferred fold of the graphs).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -39,8 +45,6 @@ namespace sw2d_dev {
 namespace {
 
 constexpr int kPX = 64;       // shared tile width: 32 lanes x 2 columns
-constexpr int kPW = 16;       // warps per CTA: warp w owns tile rows w, w + 16, ...
-constexpr int kPThreads = 32 * kPW;
 constexpr int kPFlagStride = 32;        // uints between two tiles' flags (128 B)
 constexpr int kPSmemMax = 226 * 1024;   // dynamic shared memory cap (static buffers fit beside)
 constexpr unsigned kFullMask = 0xffffffffu;
@@ -83,13 +87,14 @@ struct PAcc {
   float mx, nmn, mu, mv;
 };
 
-// K: steps per block; RW: tile rows per thread (the shared tile is 16 RW rows)
-template <int K, int RW, int RED>
-__global__ void __launch_bounds__(kPThreads)
+// K: steps per block; PW: warps per CTA (warp w owns shared rows w, w + PW,
+// ...); RW: shared rows per thread (the shared tile is PW RW rows)
+template <int K, int PW, int RW, int RED>
+__global__ void __launch_bounds__(32 * PW)
     sw2d_persist(const PersistArgs a) {
   constexpr int A = 2 * K;            // apron cells per side
   constexpr int TW = kPX - 2 * A;     // tile width
-  constexpr int Y = kPW * RW;         // shared tile rows
+  constexpr int Y = PW * RW;          // shared tile rows
   constexpr int TH = Y - 2 * A;       // tile rows
   constexpr int N = Y * kPX;
   extern __shared__ __align__(16) float psm[];
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(kPThreads)
   bool rowin[RW], rowin_n[RW];
 #pragma unroll
   for (int k = 0; k < RW; ++k) {
-    const int gj = gj0 + wp + kPW * k;
+    const int gj = gj0 + wp + PW * k;
     rowin[k] = gj >= 1 && gj <= ny;
     rowin_n[k] = gj + 1 >= 1 && gj + 1 <= ny;
     cgyr[k] = (gj >= 1 && gj < ny) ? a.c.cgy : 0.0f;
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(kPThreads)
   // initial load: the whole apron'd tile (zero outside the grid)
 #pragma unroll
   for (int k = 0; k < RW; ++k) {
-    const int y = wp + kPW * k, i = y * kPX + c0;
+    const int y = wp + PW * k, i = y * kPX + c0;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       float e = 0.0f, h0 = 0.0f, u = 0.0f, v = 0.0f;
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(kPThreads)
       // P1: h, wet; un (east faces), vn (north faces)
 #pragma unroll
       for (int k = 0; k < RW; ++k) {
-        const int y = wp + kPW * k, i = y * kPX + c0;
+        const int y = wp + PW * k, i = y * kPX + c0;
         const int iN = min(y + 1, Y - 1) * kPX + c0;   // the last row's north is stale anyway
         const float2 e2 = *reinterpret_cast<const float2*>(sE + i);
         const float2 h02 = *reinterpret_cast<const float2*>(sH0 + i);
@@ -219,7 +224,7 @@ __global__ void __launch_bounds__(kPThreads)
       // P2: etan = (E - cx (Fe - Fw)) - cy (Fn - Fs)
 #pragma unroll
       for (int k = 0; k < RW; ++k) {
-        const int y = wp + kPW * k;
+        const int y = wp + PW * k;
         const int iN = min(y + 1, Y - 1) * kPX + c0, iS = max(y - 1, 0) * kPX + c0;
         const float2 hN2 = *reinterpret_cast<const float2*>(sh + iN);
         const float2 hS2 = *reinterpret_cast<const float2*>(sh + iS);
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(kPThreads)
       acc.mv = 0.0f;
 #pragma unroll
       for (int k = 0; k < RW; ++k) {
-        const int y = wp + kPW * k, i = y * kPX + c0;
+        const int y = wp + PW * k, i = y * kPX + c0;
         const int iN = min(y + 1, Y - 1) * kPX + c0, iS = max(y - 1, 0) * kPX + c0;
         const float2 eN2 = *reinterpret_cast<const float2*>(set + iN);
         const float2 eS2 = *reinterpret_cast<const float2*>(set + iS);
@@ -294,8 +299,7 @@ __global__ void __launch_bounds__(kPThreads)
           }
         }
       }
-      if (RED >= 1) {   // CTA fold of this step's partial (deferred fold_steps)
-        __shared__ PAcc red_sh[kPW];
+      if (RED >= 1) {   // this warp's partial of the step (folded by fold_steps)
 #pragma unroll
         for (int m = 16; m >= 1; m >>= 1) {
           acc.s += __shfl_xor_sync(kFullMask, acc.s, m);
@@ -307,41 +311,34 @@ __global__ void __launch_bounds__(kPThreads)
             acc.mv = fmaxf(acc.mv, __shfl_xor_sync(kFullMask, acc.mv, m));
           }
         }
-        if (lane == 0) red_sh[wp] = acc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          PAcc t = red_sh[0];
-          for (int q2 = 1; q2 < kPW; ++q2) {
-            t.s += red_sh[q2].s;
-            t.wet += red_sh[q2].wet;
-            t.mx = fmaxf(t.mx, red_sh[q2].mx);
-            t.nmn = fmaxf(t.nmn, red_sh[q2].nmn);
-            t.mu = fmaxf(t.mu, red_sh[q2].mu);
-            t.mv = fmaxf(t.mv, red_sh[q2].mv);
-          }
+        if (lane == 0) {
           RedPartial pr;
-          pr.sum_eta = t.s;
-          pr.wet = t.wet;
-          pr.max_eta = t.mx;
-          pr.neg_min_eta = t.nmn;
-          pr.max_u = t.mu;
-          pr.max_v = t.mv;
-          a.part[(size_t)step * gridDim.x + tile] = pr;
+          pr.sum_eta = acc.s;
+          pr.wet = acc.wet;
+          pr.max_eta = acc.mx;
+          pr.neg_min_eta = acc.nmn;
+          pr.max_u = acc.mu;
+          pr.max_v = acc.mv;
+          a.part[((size_t)step * gridDim.x + tile) * PW + wp] = pr;
         }
       }
       __syncthreads();
     }
     done += kk;
     b ^= 1;
-    // publish the exact centre of the new state, then the tile's counter
+    // publish the exact centre of the new state, then the tile's counter.
+    // Between blocks the neighbours read only the centre's outer ring (A
+    // cells wide): that much is stored; after the last block all of it.
+    const bool last = done >= a.nsteps;
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
-      const int y = wp + kPW * k;
+      const int y = wp + PW * k;
       if (y < A || y >= A + TH || !rowin[k]) continue;
+      const bool yring = y < 2 * A || y >= TH;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int x = c0 + c;
-        if (x >= A && x < A + TW && colin[c]) {
+        if (x >= A && x < A + TW && colin[c] && (last || yring || x < 2 * A || x >= TW)) {
           const int i = y * kPX + x;
           const long long o = gofs(y, x);
           __stcg(a.E[b] + o, sE[i]);
@@ -350,7 +347,7 @@ __global__ void __launch_bounds__(kPThreads)
         }
       }
     }
-    if (done >= a.nsteps) break;
+    if (last) break;
     __syncthreads();
     // (the barrier orders the CTA's stores before thread 0's release, which
     // is cumulative at gpu scope)
@@ -372,7 +369,7 @@ __global__ void __launch_bounds__(kPThreads)
     // reload the apron ring (the centre is already here)
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
-      const int y = wp + kPW * k;
+      const int y = wp + PW * k;
       const bool rowc = y >= A && y < A + TH;
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -395,78 +392,96 @@ __global__ void __launch_bounds__(kPThreads)
   }
 }
 
-template <int K, int RW, int RED>
+template <int K, int PW, int RW, int RED>
 void persist_attr() {
   static unsigned long long attr_devices = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_devices >> (dev & 63) & 1ull)) {
     // (static + dynamic shared memory must stay within 227 KB per CTA)
-    cudaFuncSetAttribute(sw2d_persist<K, RW, RED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPSmemMax);
+    cudaFuncSetAttribute(sw2d_persist<K, PW, RW, RED>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemMax);
     attr_devices |= 1ull << (dev & 63);
   }
 }
 
-constexpr size_t smem_of(int rw) { return (size_t)8 * (size_t)(kPW * rw) * kPX * sizeof(float); }
+constexpr size_t smem_of(int y) { return (size_t)8 * (size_t)y * kPX * sizeof(float); }
 
-template <int K, int RW, int RED>
+template <int K, int PW, int RW, int RED>
 int capacity_t() {
-  persist_attr<K, RW, RED>();
+  persist_attr<K, PW, RW, RED>();
   int per_sm = 0, sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, RW, RED>, kPThreads,
-                                                    smem_of(RW)) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, PW, RW, RED>,
+                                                    32 * PW, smem_of(PW * RW)) != cudaSuccess) {
     cudaGetLastError();   // not sticky: the planner falls back
     return 0;
   }
   return per_sm * sms;
 }
 
-template <int K, int RW, int RED>
+template <int K, int PW, int RW, int RED>
 int launch_t(const PersistArgs& a, cudaStream_t s) {
-  persist_attr<K, RW, RED>();
+  persist_attr<K, PW, RW, RED>();
   void* args[] = {const_cast<PersistArgs*>(&a)};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)sw2d_persist<K, RW, RED>,
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)sw2d_persist<K, PW, RW, RED>,
                                                     dim3((unsigned)(a.ntx * a.nty)),
-                                                    dim3(kPThreads), args, smem_of(RW), s);
+                                                    dim3(32 * PW), args, smem_of(PW * RW), s);
   return e == cudaSuccess ? 0 : (int)e;
 }
 
-template <int K, int RW>
-int capacity_kr(int red) {
-  return red >= 2 ? capacity_t<K, RW, 2>() : red ? capacity_t<K, RW, 1>() : capacity_t<K, RW, 0>();
+// the (warps, rows per thread) shapes: 0-2: 16 warps x 1-3 rows, 3-5: 8 warps x 2-4 rows
+template <int K, int RED>
+int capacity_shape(int shape) {
+  switch (shape) {
+    case 0: return capacity_t<K, 16, 1, RED>();
+    case 1: return capacity_t<K, 16, 2, RED>();
+    case 2: return capacity_t<K, 16, 3, RED>();
+    case 3: return capacity_t<K, 8, 2, RED>();
+    case 4: return capacity_t<K, 8, 3, RED>();
+    default: return capacity_t<K, 8, 4, RED>();
+  }
 }
-template <int K, int RW>
-int launch_kr(const PersistArgs& a, int red, cudaStream_t s) {
-  return red >= 2 ? launch_t<K, RW, 2>(a, s) : red ? launch_t<K, RW, 1>(a, s)
-                                                   : launch_t<K, RW, 0>(a, s);
+template <int K, int RED>
+int launch_shape(const PersistArgs& a, cudaStream_t s) {
+  switch (a.shape) {
+    case 0: return launch_t<K, 16, 1, RED>(a, s);
+    case 1: return launch_t<K, 16, 2, RED>(a, s);
+    case 2: return launch_t<K, 16, 3, RED>(a, s);
+    case 3: return launch_t<K, 8, 2, RED>(a, s);
+    case 4: return launch_t<K, 8, 3, RED>(a, s);
+    default: return launch_t<K, 8, 4, RED>(a, s);
+  }
 }
 
 }  // namespace
 
-// tile rows per configuration: th = 16 RW - 4K (RW in {1, 2, 3})
-int persist_tile_rows(int K, int rw) { return kPW * rw - 4 * K; }
+int persist_shapes() { return 6; }
+int persist_shape_rows(int shape) {   // shared-tile rows (warps x rows per thread)
+  static const int y[6] = {16, 32, 48, 16, 24, 32};
+  return y[shape];
+}
+int persist_shape_warps(int shape) { return shape < 3 ? 16 : 8; }
+int persist_tile_rows(int K, int shape) { return persist_shape_rows(shape) - 4 * K; }
 int persist_tile_cols(int K) { return kPX - 4 * K; }
 size_t persist_flag_words(int ntiles) { return (size_t)ntiles * kPFlagStride; }
 
-int persist_capacity(int K, int red_level, int rw) {
+int persist_capacity(int K, int red_level, int shape) {
   if (K == 1)
-    return rw == 1 ? capacity_kr<1, 1>(red_level) : rw == 2 ? capacity_kr<1, 2>(red_level)
-                                                           : capacity_kr<1, 3>(red_level);
-  return rw == 1 ? capacity_kr<2, 1>(red_level) : rw == 2 ? capacity_kr<2, 2>(red_level)
-                                                         : capacity_kr<2, 3>(red_level);
+    return red_level >= 2 ? capacity_shape<1, 2>(shape)
+                          : red_level ? capacity_shape<1, 1>(shape) : capacity_shape<1, 0>(shape);
+  return red_level >= 2 ? capacity_shape<2, 2>(shape)
+                        : red_level ? capacity_shape<2, 1>(shape) : capacity_shape<2, 0>(shape);
 }
 
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  const int rw = (a.th + 4 * K) / kPW;
   if (K == 1)
-    return rw == 1 ? launch_kr<1, 1>(a, red_level, s) : rw == 2 ? launch_kr<1, 2>(a, red_level, s)
-                                                               : launch_kr<1, 3>(a, red_level, s);
-  return rw == 1 ? launch_kr<2, 1>(a, red_level, s) : rw == 2 ? launch_kr<2, 2>(a, red_level, s)
-                                                             : launch_kr<2, 3>(a, red_level, s);
+    return red_level >= 2 ? launch_shape<1, 2>(a, s)
+                          : red_level ? launch_shape<1, 1>(a, s) : launch_shape<1, 0>(a, s);
+  return red_level >= 2 ? launch_shape<2, 2>(a, s)
+                        : red_level ? launch_shape<2, 1>(a, s) : launch_shape<2, 0>(a, s);
 }
 
 }  // namespace sw2d_dev

@@ -711,12 +711,13 @@ def test_legacy_default_stream_long_run():
 # --- persistent cooperative kernel for the paper's small grids (NEXT-2) ------
 
 @pytest.mark.parametrize("k", ["1", "2"])
-@pytest.mark.parametrize("nx,ny,n,rw", [(100, 100, 100, None), (500, 500, 100, None),
-                                        (263, 97, 51, "1"), (57, 300, 20, "2"),
-                                        (1, 9, 25, None), (9, 1, 25, None), (3, 3, 7, None),
-                                        (1000, 1000, 16, None), (130, 61, 33, "3"),
-                                        (700, 90, 12, "1")])
-def test_persistent_kernel_bitwise(nx, ny, n, rw, k, monkeypatch):
+@pytest.mark.parametrize("nx,ny,n,shape", [(100, 100, 100, None), (500, 500, 100, None),
+                                           (263, 97, 51, "0"), (57, 300, 20, "1"),
+                                           (1, 9, 25, None), (9, 1, 25, None), (3, 3, 7, None),
+                                           (1000, 1000, 16, None), (130, 61, 33, "2"),
+                                           (700, 90, 12, "3"), (333, 140, 17, "4"),
+                                           (200, 257, 22, "5")])
+def test_persistent_kernel_bitwise(nx, ny, n, shape, k, monkeypatch):
     """One cooperative launch advances the whole grid: every CTA keeps its
     tile in shared memory, K steps per block, neighbour tiles synchronised by
     per-tile counters (no grid barrier, no relaunch).  Bitwise equal to the
@@ -724,8 +725,8 @@ def test_persistent_kernel_bitwise(nx, ny, n, rw, k, monkeypatch):
     diagnostics (deferred fold), chunked calls continuing the counters."""
     monkeypatch.setenv("SW2D_PERSIST", "1")
     monkeypatch.setenv("SW2D_PERSIST_K", k)
-    if rw:
-        monkeypatch.setenv("SW2D_PERSIST_RW", rw)
+    if shape:
+        monkeypatch.setenv("SW2D_PERSIST_SHAPE", shape)
     st = (si.generate(si.config("c1")) if (nx, ny) == (100, 100) else
           si.generate(si.config("c2")) if (nx, ny) == (500, 500) else
           _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny))

@@ -12,7 +12,7 @@ import sys
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_1711_04471_b200/libsw2d.so"
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 keys = ["UBLKCP", "SYNCS.ARRIVE.TRANS64", "SYNCS.PHASECHK", "LDS.128", "STG.E.128",
-        "LDG.E.128", "SHFL", "FADD2", "FMUL2", "FFMA", "FSEL", "FSETP", "IMAD.MOV", "MOV",
+        "LDG.E.128", "SHFL", "FADD2", "FMUL2", "FFMA2", "FFMA", "FSEL", "FSETP", "IMAD.MOV", "MOV",
         "HMMA", "UTCHMMA"]
 print(f"# cuobjdump -sass {lib.split('/')[-1]} (sm_100a); static instruction counts per kernel")
 for f in re.split(r"\n\s+Function : ", sass)[1:]:
