@@ -50,6 +50,7 @@ UNIT = "cell-updates/s"
 BYTES_PER_CELL = 28          # fused step: read eta,u,v,hzero (16 B) + write eta,u,v (12 B)
 PAPER_BYTES_PER_CELL = 75   # paper-shaped variant: 21 + 20 + 34 B over its 3 map kernels
 FALLBACK_HBM_GBS = 6650.0    # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+E2E_HANDLES = int(os.environ.get("SW2D_E2E_HANDLES", "3"))   # e2e pipeline depth (one GPU)
 
 
 def parse():
@@ -434,16 +435,17 @@ def run_ours(args, cfg, ws, rank, local):
         # then the result back to pinned host memory — the state eta, u, v
         # (sw2d_get_state, 12 B/cell D2H) and the T per-step volumes
         # (sw2d_reduce_history).  Wall clock around the whole loop, synchronized
-        # on both sides.  One GPU: three handles on three streams, pipelined
-        # the way a user runs a stream of problems — problem k+1 uploads and
-        # problem k-1 downloads (two host threads; the calls block) while
-        # problem k computes; the computes are serialised by events, so
-        # compute never overlaps compute.  Several ranks: one handle, serial.
+        # on both sides.  One GPU: SW2D_E2E_HANDLES (default 3) handles on as
+        # many streams, pipelined the way a user runs a stream of problems —
+        # problem k+1 uploads and problem k-1 downloads (two host threads; the
+        # calls block) while problem k computes; the computes are serialised by
+        # events, so compute never overlaps compute.  Several ranks: one
+        # handle, serial.
         e2e = None
         if not args.no_e2e and not args.profile:
             out_state = [[torch.empty((nrows, nx), dtype=torch.float32, pin_memory=True)
-                          for _ in range(3)] for _ in range(3)]
-            out_hist = [np.empty(max(T, 1), np.float64) for _ in range(3)]
+                          for _ in range(3)] for _ in range(E2E_HANDLES)]
+            out_hist = [np.empty(max(T, 1), np.float64) for _ in range(E2E_HANDLES)]
 
             def read_back(hh, b):
                 sw2d.sw2d_get_state(hh, *out_state[b])
@@ -467,7 +469,7 @@ def run_ours(args, cfg, ws, rank, local):
             wall, how = wall_serial, "serial, one handle"
             if ws == 1:
                 import threading
-                nh = 3
+                nh = E2E_HANDLES
                 streams = [stream] + [torch.cuda.Stream() for _ in range(nh - 1)]
                 hs = [h] + [sw2d.sw2d_create(p, sw2d.make_dist(rank, ws, local, 0, uid, halo), st)
                             for st in streams[1:]]
@@ -522,7 +524,8 @@ def run_ours(args, cfg, ws, rank, local):
                     wall = time.perf_counter() - t0
                     if err:
                         raise err[0]
-                    how = "pipelined: three handles on three streams, upload / compute / download"
+                    how = (f"pipelined: {nh} handles on {nh} streams, upload / compute / "
+                           "download")
                     last = (args.steps - 1) % nh
                     assert torch.equal(out_state[last][0], ref_eta), "e2e: handles disagree"
                 finally:

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -26,6 +27,9 @@ using namespace sw2d_dev;
 namespace {
 
 thread_local std::string t_create_err;
+
+std::mutex g_persist_mu;                  // orders persistent launches per device
+cudaEvent_t g_persist_last[64] = {};
 
 constexpr long long kSmallMaxCells = 1LL << 21;   // small-grid kernel up to ~1448^2
 constexpr int kMinRowsPerSeg = 4;
@@ -310,8 +314,8 @@ float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch;
 // Small grids: the persistent cooperative kernel (sw2d_persist.cu), on one
 // GPU without ranks, if its tiles fit co-resident.  By default where it
 // measured faster than the graph-replayed row march: up to
-// 2^18 cells (C1 1.55 vs 2.49 us/step, C2 3.25 vs 3.62; with VOLUME per step
-// 1.96 vs 2.92 and 3.54 vs 3.94); SW2D_PERSIST=0/1 forces it off/on (on: up
+// 2^18 cells (C1 1.57 vs 2.62 us/step, C2 3.05 vs 3.68; with VOLUME per step
+// 1.92 vs 3.02 and 3.59 vs 4.00); SW2D_PERSIST=0/1 forces it off/on (on: up
 // to 2^21 cells).  K = 2 steps per block (SW2D_PERSIST_K); the CTA shape
 // (warps x rows per thread; SW2D_PERSIST_SHAPE) minimises the busiest SM's
 // work, see below.
@@ -345,10 +349,15 @@ void plan_persist(sw2d* h) {
     const long long nt = (long long)ntx * nty;
     if (nt > persist_capacity(K, h->red_level, sh)) continue;
     // the busiest SM's shared rows; a lone CTA per SM counted 1.5x (nothing
-    // overlaps its handshake).  Measured on C2: 8 warps x 24 rows, 288 tiles
-    // (2 per SM) 3.18 us/step; 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
+    // overlaps its handshake), four or more (without the per-step partials'
+    // registers) 2/3 (they hide each other's latency).  Measured on C2
+    // (profiles/ab_r02q.log): 8 warps x 16 rows, 567 tiles (4 per SM) 3.03
+    // us/step, 8 x 24, 288 tiles 3.17 (3.58 vs 3.76 with VOLUME per step);
+    // 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
     const long long per_sm = (nt + sms - 1) / sms;
-    const double cost = (double)persist_shape_rows(sh) * (per_sm == 1 ? 1.5 : (double)per_sm);
+    const double cost = (double)persist_shape_rows(sh) * (double)per_sm *
+                        (per_sm == 1 ? 1.5 : 1.0) *
+                        (per_sm >= 4 && h->red_level == 0 ? 2.0 / 3.0 : 1.0);
     if (best < 0 || cost < best - 1e-9) {
       best = cost;
       h->pk = K;
@@ -1598,7 +1607,19 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
         set_dstep<<<1, 1, 0, h->stream>>>(h->dstep, (unsigned long long)h->steps);
         h->nlaunch++;
       }
-      const int e = launch_persist(a, h->pk, h->red_level, h->stream);
+      int e = 0;
+      {
+        // persistent launches of all handles of this process on this device
+        // run one after another: two of them side by side could each hold
+        // part of the SMs while their resident CTAs wait on tiles that
+        // cannot start
+        std::lock_guard<std::mutex> lk(g_persist_mu);
+        cudaEvent_t& last = g_persist_last[h->device & 63];
+        if (!last) CUDA_TRY(h, cudaEventCreateWithFlags(&last, cudaEventDisableTiming));
+        CUDA_TRY(h, cudaStreamWaitEvent(h->stream, last, 0));
+        e = launch_persist(a, h->pk, h->red_level, h->stream);
+        if (!e) CUDA_TRY(h, cudaEventRecord(last, h->stream));
+      }
       if (e) return fail(h, SW2D_ECUDA, std::string("cooperative launch: ") +
                                             cudaGetErrorString((cudaError_t)e));
       h->nlaunch++;

@@ -89,8 +89,10 @@ struct PAcc {
 
 // K: steps per block; PW: warps per CTA (warp w owns shared rows w, w + PW,
 // ...); RW: shared rows per thread (the shared tile is PW RW rows)
+// (8 warps x 2 rows: at most 64 registers, so 4 CTAs fit an SM; 16 warps:
+// 64, so 2 fit)
 template <int K, int PW, int RW, int RED>
-__global__ void __launch_bounds__(32 * PW)
+__global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 ? 2 : 1))
     sw2d_persist(const PersistArgs a) {
   constexpr int A = 2 * K;            // apron cells per side
   constexpr int TW = kPX - 2 * A;     // tile width

@@ -768,3 +768,27 @@ def test_persistent_kernel_long_run_history(history_len, monkeypatch):
     got, hist = _history_run(st, [3, 254], ALL, history_len)
     assert_state_equal(got, want[:4], where=f"persistent long run, history {history_len}")
     _check_history(hist, want[4], n)
+
+
+def test_persistent_kernels_of_two_handles_interleave_safely():
+    """Two small-grid handles on their own streams, stepped back to back
+    without synchronisation: their persistent launches are ordered (one
+    device-wide event), so neither waits on CTAs the other keeps from
+    starting; both equal the oracle."""
+    st = si.generate(si.config("c1"))
+    want = oracle_run(P, st, 150)
+    hs = []
+    try:
+        for _ in range(2):
+            h = sw2d.sw2d_create(sw2d.make_params(100, 100, reduce_every_step=1, history_len=8))
+            assert "kernel=persist" in sw2d.sw2d_plan(h), sw2d.sw2d_plan(h)
+            sw2d.sw2d_set_state(h, *st)
+            hs.append(h)
+        for chunk in (64, 86):
+            for h in hs:
+                sw2d.sw2d_step(h, chunk)
+        for h in hs:
+            assert_state_equal(sw2d.get_state(h, 100), want, where="two handles")
+    finally:
+        for h in hs:
+            sw2d.sw2d_destroy(h)
