@@ -92,6 +92,22 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def l2_peak():
+    """The L2 roofline's peak: the best copy bandwidth over L2-resident
+    footprints (<= 64 MB) measured by tools/l2_bw.cu on a B200
+    (profiles/r02_l2_peak.json), or (None, why)."""
+    p = os.path.join(ROOT, "profiles", "r02_l2_peak.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        best = max(r["gbs"] for r in d["results"]
+                   if r["kind"] == "copy" and r["footprint_mb"] <= 64)
+        return float(best), ("measured: tools/l2_bw.cu copy kernel, L2-resident footprint "
+                             "(profiles/r02_l2_peak.json)")
+    except Exception as e:  # noqa: BLE001
+        return None, "no L2 measurement (%s)" % type(e).__name__
+
+
 def _ncu_summary():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -364,14 +380,25 @@ def run_ours(args, cfg, ws, rank, local):
         red_lvl = 0 if not mask else (1 if mask < 4 else 2)
         launches_per_step = launches / (T * args.steps)
         plan = dict(kv.split("=") for kv in sw2d.sw2d_plan(h).split())
-        spl = int(plan.get("steps_per_launch", "1")) if args.variant == "fused" else 1
+        persist = plan.get("kernel") == "persist"
+        pk = int(plan.get("steps_per_block", "0"))
+        if persist:
+            # K steps per shared-memory block; the bytes are those of the
+            # two-step pass (14 B/cell-step), whatever K, so that the small-grid
+            # kernels compare on one scale
+            spl = 2
+        else:
+            spl = int(plan.get("steps_per_launch", "1")) if args.variant == "fused" else 1
         t_launch_s = ms * 1e-3 / (T * args.steps) * spl
         cells_local = nrows * nx
         bpc = BYTES_PER_CELL if args.variant == "fused" else PAPER_BYTES_PER_CELL
         alg_bytes = bpc * cells_local            # state in + state out, per launch
         hbm_achieved = alg_bytes / t_launch_s / 1e9
         peak, peak_src = hbm_peak()
-        if plan.get("kernel") == "small":
+        if persist:
+            kname = "sw2d_persist<%d, %s, %s, %d>" % (pk, plan["warps"], plan["rows_per_thread"],
+                                                      red_lvl)
+        elif plan.get("kernel") == "small":
             kname = ("sw2d_step_small2<%d>" if spl == 2 else "sw2d_step_small<%d>") % red_lvl
         elif spl == 2:
             kname = "sw2d_step_cta2<%d>" % red_lvl
@@ -393,6 +420,27 @@ def run_ours(args, cfg, ws, rank, local):
                 "algorithmic_bytes_per_cell_step": bpc / spl, "model_steps_per_launch": spl,
                 "kernel": kname, "launches_per_model_step": launches_per_step,
                 "plan": sw2d.sw2d_plan(h)}
+        if persist or plan.get("kernel") == "small":
+            # Small grids (state in L2, the persistent kernel or the small-grid
+            # graphs): the same algorithmic bytes — what a two-step pass must
+            # move in and out, 14 B/cell-step — can only come from L2, so the
+            # roofline is L2's measured copy bandwidth (tools/l2_bw.cu); the
+            # HBM figures move to hbm_view.
+            # (The persistent kernel keeps its tile in shared memory and moves
+            # only the tile rings through L2, so this bounds the regime, not
+            # the kernel's own traffic: a low frac = latency-bound.)
+            l2, l2_src = l2_peak()
+            if l2:
+                hv = {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac",
+                                           "peak_source", "traffic")}
+                roof.update(bound="l2", peak=l2, frac=hbm_achieved / l2, peak_source=l2_src,
+                            traffic=None, hbm_view=hv)
+            roof["us_per_model_step"] = ms * 1e3 / (T * args.steps)
+        if persist:   # one launch runs many blocks of K steps
+            roof["algorithmic_bytes_per_two_steps"] = roof.pop("algorithmic_bytes_per_launch")
+            roof.pop("model_steps_per_launch")
+            roof["model_steps_per_block"] = pk
+            roof["launches_per_model_step"] = launches_per_step
         # the survey's single-step budget (28 B per cell-STEP):
         # above 1 here because two steps share one HBM pass
         roof["survey_28B_frac"] = value / ws * BYTES_PER_CELL / 1e9 / peak

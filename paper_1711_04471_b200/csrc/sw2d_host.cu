@@ -333,40 +333,66 @@ void plan_persist(sw2d* h) {
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  int K = 2;
-  if (const char* e = std::getenv("SW2D_PERSIST_K")) K = std::atoi(e) == 1 ? 1 : 2;
+  int K_force = 0;
+  if (const char* e = std::getenv("SW2D_PERSIST_K")) K_force = std::max(1, std::min(4, std::atoi(e)));
   int shape_force = -1;
   if (const char* e = std::getenv("SW2D_PERSIST_SHAPE"))
     shape_force = std::max(0, std::min(persist_shapes() - 1, std::atoi(e)));
-  const int tw = persist_tile_cols(K);
-  const int ntx = (int)((h->p.nx + tw - 1) / tw);
-  // the shape that minimises the busiest SM's work (ties: the first, more warps)
-  double best = -1;
-  for (int sh = 0; sh < persist_shapes(); ++sh) {
-    if (shape_force >= 0 && sh != shape_force) continue;
-    const int th = persist_tile_rows(K, sh);
-    const int nty = (int)((h->p.ny + th - 1) / th);
-    const long long nt = (long long)ntx * nty;
-    if (nt > persist_capacity(K, h->red_level, sh)) continue;
-    // the busiest SM's shared rows; a lone CTA per SM counted 1.5x (nothing
-    // overlaps its handshake), four or more (without the per-step partials'
-    // registers) 2/3 (they hide each other's latency).  Measured on C2
-    // (profiles/ab_r02q.log): 8 warps x 16 rows, 567 tiles (4 per SM) 3.03
-    // us/step, 8 x 24, 288 tiles 3.17 (3.58 vs 3.76 with VOLUME per step);
-    // 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
-    const long long per_sm = (nt + sms - 1) / sms;
-    const double cost = (double)persist_shape_rows(sh) * (double)per_sm *
-                        (per_sm == 1 ? 1.5 : 1.0) *
-                        (per_sm >= 4 && h->red_level == 0 ? 2.0 / 3.0 : 1.0);
-    if (best < 0 || cost < best - 1e-9) {
-      best = cost;
-      h->pk = K;
-      h->pshape = sh;
-      h->pth = th;
-      h->pntx = ntx;
-      h->pnty = nty;
+  struct Pick { int shape = -1, th = 0, ntx = 0, nty = 0; long long per_sm = 0; double cost = -1; };
+  // the shape that minimises the busiest SM's work for K steps per block
+  // (ties: the first, more warps)
+  auto pick = [&](int K) {
+    Pick best;
+    const int tw = persist_tile_cols(K);
+    const int ntx = (int)((h->p.nx + tw - 1) / tw);
+    for (int sh = 0; sh < persist_shapes(); ++sh) {
+      if (shape_force >= 0 && sh != shape_force) continue;
+      const int th = persist_tile_rows(K, sh);
+      if (th <= 0) continue;
+      const int nty = (int)((h->p.ny + th - 1) / th);
+      const long long nt = (long long)ntx * nty;
+      if (nt > persist_capacity(K, h->red_level, sh)) continue;
+      // the busiest SM's shared rows; a lone CTA per SM counted 1.5x (nothing
+      // overlaps its handshake), four or more (without the per-step partials'
+      // registers) 2/3 (they hide each other's latency).  Measured on C2
+      // (profiles/ab_r02q.log): 8 warps x 16 rows, 567 tiles (4 per SM) 3.03
+      // us/step, 8 x 24, 288 tiles 3.17 (3.58 vs 3.76 with VOLUME per step);
+      // 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
+      const long long per_sm = (nt + sms - 1) / sms;
+      const double cost = (double)persist_shape_rows(sh) * (double)per_sm *
+                          (per_sm == 1 ? 1.5 : 1.0) *
+                          (per_sm >= 4 && h->red_level == 0 ? 2.0 / 3.0 : 1.0);
+      if (best.cost < 0 || cost < best.cost - 1e-9) {
+        best.shape = sh;
+        best.th = th;
+        best.ntx = ntx;
+        best.nty = nty;
+        best.per_sm = per_sm;
+        best.cost = cost;
+      }
+    }
+    return best;
+  };
+  // K: 2, or 3 where the grid keeps several CTAs on every SM and no per-step
+  // partials are written (one handshake per three steps then pays for the
+  // wider apron: C2 3.03 -> 2.85 us/step with 16 warps x 32 rows; with a
+  // lone CTA per SM (C1) the phases' latency dominates and K = 3 is slower,
+  // 1.58 -> 2.07; with VOLUME per step within +-3%: profiles/ab_r02v.log)
+  int K = K_force ? K_force : 2;
+  Pick p = pick(K);
+  if (!K_force && h->red_level == 0 && p.shape >= 0 && p.per_sm >= 2) {
+    const Pick p3 = pick(3);
+    if (p3.shape >= 0) {
+      K = 3;
+      p = p3;
     }
   }
+  if (p.shape < 0) return;
+  h->pk = K;
+  h->pshape = p.shape;
+  h->pth = p.th;
+  h->pntx = p.ntx;
+  h->pnty = p.nty;
 }
 
 void plan_launches(sw2d* h) {
@@ -485,9 +511,10 @@ void plan_launches(sw2d* h) {
     if (h->pk) {
       std::snprintf(buf, sizeof(buf),
                     "kernel=persist steps_per_block=%d tiles=%dx%d tile=%dx%d warps=%d "
-                    "cooperative=1 halo=%s",
+                    "rows_per_thread=%d cooperative=1 halo=%s",
                     h->pk, h->pntx, h->pnty, persist_tile_cols(h->pk), h->pth,
                     persist_shape_warps(h->pshape),
+                    persist_shape_rows(h->pshape) / persist_shape_warps(h->pshape),
                     h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl");
       h->plan_text = buf;
     }

@@ -465,25 +465,47 @@ int persist_shape_rows(int shape) {   // shared-tile rows (warps x rows per thre
   return y[shape];
 }
 int persist_shape_warps(int shape) { return shape < 3 ? 16 : 8; }
-int persist_tile_rows(int K, int shape) { return persist_shape_rows(shape) - 4 * K; }
+// a tile must be at least as tall as the apron (2K rows), or the apron would
+// reach past the neighbour tile whose counter is awaited: 0 = shape unusable
+int persist_tile_rows(int K, int shape) {
+  const int th = persist_shape_rows(shape) - 4 * K;
+  return th >= 2 * K ? th : 0;
+}
 int persist_tile_cols(int K) { return kPX - 4 * K; }
 size_t persist_flag_words(int ntiles) { return (size_t)ntiles * kPFlagStride; }
 
+// K = 3, 4 need more than 16 shared rows: shapes 0 and 3 have no usable tile
+// rows then (the planner skips them: persist_tile_rows <= 0)
+template <int K>
+int capacity_k(int red_level, int shape) {
+  if (persist_tile_rows(K, shape) <= 0) return 0;
+  return red_level >= 2 ? capacity_shape<K, 2>(shape)
+                        : red_level ? capacity_shape<K, 1>(shape) : capacity_shape<K, 0>(shape);
+}
+template <int K>
+int launch_k(const PersistArgs& a, int red_level, cudaStream_t s) {
+  return red_level >= 2 ? launch_shape<K, 2>(a, s)
+                        : red_level ? launch_shape<K, 1>(a, s) : launch_shape<K, 0>(a, s);
+}
+
 int persist_capacity(int K, int red_level, int shape) {
-  if (K == 1)
-    return red_level >= 2 ? capacity_shape<1, 2>(shape)
-                          : red_level ? capacity_shape<1, 1>(shape) : capacity_shape<1, 0>(shape);
-  return red_level >= 2 ? capacity_shape<2, 2>(shape)
-                        : red_level ? capacity_shape<2, 1>(shape) : capacity_shape<2, 0>(shape);
+  switch (K) {
+    case 1: return capacity_k<1>(red_level, shape);
+    case 3: return capacity_k<3>(red_level, shape);
+    case 4: return capacity_k<4>(red_level, shape);
+    default: return capacity_k<2>(red_level, shape);
+  }
 }
 
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (K == 1)
-    return red_level >= 2 ? launch_shape<1, 2>(a, s)
-                          : red_level ? launch_shape<1, 1>(a, s) : launch_shape<1, 0>(a, s);
-  return red_level >= 2 ? launch_shape<2, 2>(a, s)
-                        : red_level ? launch_shape<2, 1>(a, s) : launch_shape<2, 0>(a, s);
+  if (persist_tile_rows(K, a.shape) <= 0) return (int)cudaErrorInvalidValue;
+  switch (K) {
+    case 1: return launch_k<1>(a, red_level, s);
+    case 3: return launch_k<3>(a, red_level, s);
+    case 4: return launch_k<4>(a, red_level, s);
+    default: return launch_k<2>(a, red_level, s);
+  }
 }
 
 }  // namespace sw2d_dev
