@@ -491,9 +491,10 @@ def run_ours(args, cfg, ws, rank, local):
         # handle, serial.
         e2e = None
         if not args.no_e2e and not args.profile:
+            nbuf = E2E_HANDLES if ws == 1 else 1   # (several ranks: one handle, serial)
             out_state = [[torch.empty((nrows, nx), dtype=torch.float32, pin_memory=True)
-                          for _ in range(3)] for _ in range(E2E_HANDLES)]
-            out_hist = [np.empty(max(T, 1), np.float64) for _ in range(E2E_HANDLES)]
+                          for _ in range(3)] for _ in range(nbuf)]
+            out_hist = [np.empty(max(T, 1), np.float64) for _ in range(nbuf)]
 
             def read_back(hh, b):
                 sw2d.sw2d_get_state(hh, *out_state[b])
