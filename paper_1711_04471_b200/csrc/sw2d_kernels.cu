@@ -347,6 +347,9 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 // predicate program the rule is (two compares with a predicate combine, one
 // 3-input predicate op, one select); ptxas otherwise if-converts it into a
 // chain of selects
+#ifndef SW2D_FACE_ARITH
+#define SW2D_FACE_ARITH 1   // 0: the predicate program below (A/B)
+#endif
 __device__ __forceinline__ float face_sel(float wc, float wn, float d, float s) {
   float r;
   asm("{\n\t.reg .pred pc, pn, pa, pb;\n\t"
@@ -574,15 +577,43 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   for (int c = 0; c < C; ++c) cg[c] = x.cgxc[c];
   vmul<C, kPack>(du, cg, du, x.nz);
   vsub<C, kPack>(dv, eL, w.e);
+#if SW2D_FACE_ARITH
+  // north / south wall rows: coefficient 0, so dv = 0 and the face rule
+  // below blocks the face (one side is outside the grid, dry)
+  vmul<C, kPack>(dv, vrow ? x.cgy : 0.0f, dv, x.nz);
+#else
   vmul<C, kPack>(dv, x.cgy, dv, x.nz);
+#endif
   vadd<C, kPack>(su, uL, du);
   vadd<C, kPack>(sv, w.v, dv);
+#if SW2D_FACE_ARITH
+  // The face rule as exact arithmetic (R26): with wet flags wc, wn in {0, 1},
+  // f = wc*wn + (wc - wn)*d is exactly 1 (both wet), d (only wc), -d (only wn)
+  // or a zero (neither), so the face carries flow iff f > 0 — the rule of
+  // R4 — and every operation here is exact (no rounding): packed pairs, one
+  // compare and one select per face instead of a predicate program.
+  float wnE[C], fu[C], fv[C], tq[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) wnE[c] = (c < C - 1) ? wL[c + 1] : wR;
+  vsub<C, kPackS>(tq, wL, wnE);
+  vmul<C, kPack>(tq, tq, du, x.nz);
+  vselfma<C, kPackS>(fu, wL, wnE, tq);
+  vsub<C, kPack>(tq, w.w1, wL);
+  vmul<C, kPack>(tq, tq, dv, x.nz);
+  vselfma<C, kPack>(fv, w.w1, wL, tq);
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    un[c] = fu[c] > 0.0f ? su[c] : 0.0f;
+    vn[c] = fv[c] > 0.0f ? sv[c] : 0.0f;
+  }
+#else
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const float wn = (c < C - 1) ? wL[c + 1] : wR;
     un[c] = face_sel(wL[c], wn, du[c], su[c]);
     vn[c] = vrow ? face_sel(w.w1[c], wL[c], dv[c], sv[c]) : 0.0f;
   }
+#endif
 
   // a3: fluxes of row L-1 and etan(L-1)
   float hx[C], hy[C], fx[C], fy[C], et[C];
