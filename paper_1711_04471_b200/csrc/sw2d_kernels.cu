@@ -350,6 +350,7 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 #ifndef SW2D_FACE_ARITH
 #define SW2D_FACE_ARITH 1   // 0: the predicate program below (A/B)
 #endif
+#if !SW2D_FACE_ARITH
 __device__ __forceinline__ float face_sel(float wc, float wn, float d, float s) {
   float r;
   asm("{\n\t.reg .pred pc, pn, pa, pb;\n\t"
@@ -364,6 +365,7 @@ __device__ __forceinline__ float face_sel(float wc, float wn, float d, float s) 
       : "f"(wc), "f"(wn), "f"(d), "f"(s));
   return r;
 }
+#endif
 
 
 // Column-parallel FP32 arithmetic on C-column arrays.  sm_100a issues the

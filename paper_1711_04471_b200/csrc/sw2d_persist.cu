@@ -59,8 +59,20 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// the face rule's predicate program (as in the row march): flow ? s : 0
+#ifndef SW2D_PERSIST_FACE_ARITH
+#define SW2D_PERSIST_FACE_ARITH 1
+#endif
+// the face rule (R4) as exact arithmetic (R26, as in the row march): with
+// flags wc, wn in {0, 1}, wc*wn + (wc - wn)*d > 0 iff the face carries flow
+__device__ __forceinline__ float p_face_arith(float wc, float wn, float d, float s) {
+  const float f = __fmaf_rn(wc, wn, __fmul_rn(__fsub_rn(wc, wn), d));
+  return f > 0.0f ? s : 0.0f;
+}
+// the face rule's predicate program: flow ? s : 0
 __device__ __forceinline__ float p_face(float wc, float wn, float d, float s) {
+#if SW2D_PERSIST_FACE_ARITH
+  return p_face_arith(wc, wn, d, s);
+#else
   float r;
   asm("{\n\t.reg .pred pc, pn, pa, pb;\n\t"
       "setp.ne.f32 pc, %1, 0f00000000;\n\t"
@@ -73,6 +85,7 @@ __device__ __forceinline__ float p_face(float wc, float wn, float d, float s) {
       : "=f"(r)
       : "f"(wc), "f"(wn), "f"(d), "f"(s));
   return r;
+#endif
 }
 
 // upwind flux s * (s > 0 ? hl : hr): equal in value to the oracle's
