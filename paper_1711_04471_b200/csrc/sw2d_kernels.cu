@@ -979,6 +979,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 #ifndef SW2D_CTA2_PIPE
 #define SW2D_CTA2_PIPE 2      // second march one row behind (A/B builds: 0, 1)
 #endif
+#ifndef SW2D_CTA2_PIPE_ALL
+#define SW2D_CTA2_PIPE_ALL 1  // the pipelined pair without diagnostics too (A/B: 0)
+#endif
 #ifndef SW2D_CTA2_UNROLL3
 #define SW2D_CTA2_UNROLL3 1   // (without PIPE) 0: the two-row loop
 #endif
@@ -1107,9 +1110,9 @@ constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
 template <int RED, bool REMOTE>
 __global__ void __launch_bounds__(kCta2Threads, 1)
     sw2d_step_cta2(const StepArgs a) {
-  // with per-step diagnostics the pipelined pair is faster (C5 VOLUME +1%,
-  // all seven +0.5%); without them the plain pair (-2% pipelined)
-  constexpr bool kPipe = SW2D_CTA2_PIPE && RED >= 1;
+  // the pipelined pair (C5 VOLUME +1%, all seven +0.5%; without diagnostics
+  // +0.7% since the face rule became arithmetic, -2% before)
+  constexpr bool kPipe = SW2D_CTA2_PIPE && (RED >= 1 || SW2D_CTA2_PIPE_ALL);
   extern __shared__ __align__(128) unsigned char dsm[];
   unsigned char* ring = dsm;
   const uint32_t sring = smem_u32(ring);
