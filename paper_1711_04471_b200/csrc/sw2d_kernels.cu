@@ -26,6 +26,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <type_traits>
 
 #include "sw2d_internal.cuh"
 
@@ -532,7 +533,9 @@ struct RowOut {
 // STORE: write the outputs of this segment's rows to global memory; else
 // return them in `out` (the first step of a two-step pass keeps its state in
 // registers).  The diagnostics of the segment's rows are accumulated either way.
-template <int RED, bool REMOTE, int C, bool STORE = true>
+// EDGE = false: the caller guarantees that rows L-2 .. L are output rows of
+// the segment inside 1..ny (and L-1 is not a wall row): no row tests.
+template <int RED, bool REMOTE, int C, bool STORE = true, bool EDGE = true>
 __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const float (&eL)[C],
                                          const float (&h0L)[C], const float (&uL)[C],
                                          const float (&vL)[C], const int L, const Ctx& x,
@@ -548,7 +551,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   constexpr bool kPack = RED >= SW2D_F32X2_MIN_RED;
   // the pairs with a neighbour-shifted operand (they need IMAD.MOV to align)
   constexpr bool kPackS = kPack && SW2D_F32X2_SHIFTED;
-  const bool rowok = in_rows(L, 1, x.ny);
+  const bool rowok = !EDGE || in_rows(L, 1, x.ny);
   float hL[C], wL[C];
   vadd<C, kPack>(hL, h0L, eL);
 #pragma unroll
@@ -567,7 +570,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   // other face keeps cgx and the arithmetic of §4.  (The same trick per row
   // for the north/south walls made ptxas emit more selects: the row select
   // stays.)
-  const bool vrow = (L - 1 >= 1) && (L - 1 < x.ny);  // not the north / south wall
+  const bool vrow = !EDGE || ((L - 1 >= 1) && (L - 1 < x.ny));  // not the north / south wall
   // (the arithmetic below is column-parallel: vadd / vsub / vmul, same
   // operations and operand order as the scalar form)
   float en[C], du[C], dv[C], su[C], sv[C], un[C], vn[C];
@@ -670,7 +673,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
 
   // a5: commit (lanes 1..30, rows of this segment)
   if (x.out_lane) {
-    if (in_rows(L, x.ra, x.rb)) {
+    if (!EDGE || in_rows(L, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
       if constexpr (STORE) SW2D_CHECK(pU >= x.dU && pU + C <= x.dU + x.nelem);
 #endif
@@ -681,7 +684,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
         for (int c = 0; c < C; ++c) acc.max_u = fmaxf(acc.max_u, fabsf(un[c]));
       }
     }
-    if (in_rows(L - 1, x.ra, x.rb)) {
+    if (!EDGE || in_rows(L - 1, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
       if constexpr (STORE) SW2D_CHECK(pV >= x.dV && pV + C <= x.dV + x.nelem);
 #endif
@@ -692,7 +695,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
         for (int c = 0; c < C; ++c) acc.max_v = fmaxf(acc.max_v, fabsf(vn[c]));
       }
     }
-    if (in_rows(L - 2, x.ra, x.rb)) {
+    if (!EDGE || in_rows(L - 2, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
       if constexpr (STORE) SW2D_CHECK(pE >= x.dE && pE + C <= x.dE + x.nelem);
 #endif
@@ -978,6 +981,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
 // --- Two steps per pass (the CTA ring kernel, single slab) ------------------
 #ifndef SW2D_CTA2_PIPE
 #define SW2D_CTA2_PIPE 2      // second march one row behind (A/B builds: 0, 1)
+#endif
+#ifndef SW2D_CTA2_INTERIOR
+#define SW2D_CTA2_INTERIOR 1  // a row loop without row tests between the segment's edges
 #endif
 #ifndef SW2D_CTA2_PIPE_ALL
 #define SW2D_CTA2_PIPE_ALL 1  // the pipelined pair without diagnostics too (A/B: 0)
@@ -1300,11 +1306,15 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
       // per row: march 2 (row L-3, from the slots) first, then the row's
       // fetch straight into the hzero slot it just consumed (no copy; the
       // shared-memory loads run under march 2's arithmetic), then march 1
-      auto phase = [&](Win2<4>& w, Win2<4>& ow, int ii, long long o, float (&uS)[4],
-                       float (&hS)[4], const float (&vIn)[4], float (&vOut)[4]) {
+      // (edge: std::true_type on the segment's first and last rows, whose
+      // outputs may fall outside it or the grid; false_type in between)
+      auto phase = [&](auto edge, Win2<4>& w, Win2<4>& ow, int ii, long long o, float (&uS)[4],
+                       float (&hS)[4], const float (&vIn)[4],
+                       float (&vOut)[4]) __attribute__((always_inline)) {
+        constexpr bool kEdge = decltype(edge)::value;
         const int L = first + ii;
-        row_stepC<RED, REMOTE, 4, true>(w.s2, ow.s2, e1, hS, uS, vIn, L - 3, x, acc2, Un + o,
-                                        Vn + o - pitch, En + o - 2 * pitch);
+        row_stepC<RED, REMOTE, 4, true, kEdge>(w.s2, ow.s2, e1, hS, uS, vIn, L - 3, x, acc2,
+                                               Un + o, Vn + o - pitch, En + o - 2 * pitch);
         float4 E4, H4, U4, V4;
         fetch(ii, E4, H4, U4, V4);
         const float eL[4] = {E4.x, E4.y, E4.z, E4.w};
@@ -1312,8 +1322,8 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
         const float vL[4] = {V4.x, V4.y, V4.z, V4.w};
         hS[0] = H4.x; hS[1] = H4.y; hS[2] = H4.z; hS[3] = H4.w;
         RowOut<4> r1;
-        row_stepC<RED, false, 4, false>(w.s1, ow.s1, eL, hS, uL, vL, L, x, acc1, nullptr,
-                                        nullptr, nullptr, &r1);
+        row_stepC<RED, false, 4, false, kEdge>(w.s1, ow.s1, eL, hS, uL, vL, L, x, acc1, nullptr,
+                                               nullptr, nullptr, &r1);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uS[c] = r1.un[c];
@@ -1321,12 +1331,20 @@ __global__ void __launch_bounds__(kCta2Threads, 1)
           e1[c] = r1.En[c];
         }
       };
-      for (; i + 2 < n; i += 3) {
+      auto three = [&](auto edge) __attribute__((always_inline)) {
         const long long o = lo + (long long)(i - 3) * pitch;   // row first + i - 3
-        phase(wa, wb, i, o, uA, hA, vB, vA);
-        phase(wb, wc, i + 1, o + pitch, uB, hB, vC, vB);
-        phase(wc, wa, i + 2, o + 2 * pitch, uC, hC, vA, vC);
-      }
+        phase(edge, wa, wb, i, o, uA, hA, vB, vA);
+        phase(edge, wb, wc, i + 1, o + pitch, uB, hB, vC, vB);
+        phase(edge, wc, wa, i + 2, o + 2 * pitch, uC, hC, vA, vC);
+      };
+#if SW2D_CTA2_INTERIOR
+      // row L = first + i writes u'(L-3), v'(L-4), eta'(L-5) (march 2) and
+      // folds rows L .. L-2 of march 1: all of them segment rows (ra = first
+      // + 4 .. rb = first + n - 6, inside 1..ny) for 9 <= i <= n - 6
+      for (; i + 2 < n && i < 9; i += 3) three(std::true_type{});
+      for (; i + 2 < n - 5; i += 3) three(std::false_type{});
+#endif
+      for (; i + 2 < n; i += 3) three(std::true_type{});
 #else
       for (; i + 2 < n; i += 3) {
         float4 E4, H4, U4, V4;
