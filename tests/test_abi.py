@@ -45,22 +45,42 @@ def test_built_for_sm100a(lib):
     assert "sm_100a" in out
 
 
+_PROBE_DEFINES = (("-DSW2D_EXACT_FMA=0", "-DSW2D_F32X2_MIN_RED=0"),
+                  ("-DSW2D_EXACT_FMA=0", "-DSW2D_PACKED_MUL=0"))
+_probe_cache = {}
+
+
+def _probe_cmd(red, defines, cubin):
+    from paper_1711_04471_b200 import _build
+    cmd = [_build.NVCC, *[f for f in _build.FLAGS if f not in ("-shared",)],
+           "-Xcompiler", "-fPIC", f"-DPROBE_RED={red}", *defines,
+           "-I", os.path.join(ROOT, "include"), "-I", _build.CSRC, "-cubin", "-o", cubin,
+           os.path.join(ROOT, "tools", "cta2_probe.cu")]
+    return [c for c in cmd if c != "-Xcompiler,-fPIC,-O2,-Wall"]
+
+
 def _probe_sass(red, *defines):
     """SASS of sw2d_step_cta2<red, 0> alone (tools/cta2_probe.cu), built with the
-    library's flags plus `defines`."""
+    library's flags plus `defines`.  The first call builds every (red, defines)
+    pair the tests use at once, in parallel (each takes tens of seconds)."""
     import subprocess
     import tempfile
-    with tempfile.TemporaryDirectory() as d:
-        cubin = os.path.join(d, "probe.cubin")
-        from paper_1711_04471_b200 import _build
-        cmd = [_build.NVCC, *[f for f in _build.FLAGS if f not in ("-shared",)],
-               "-Xcompiler", "-fPIC", f"-DPROBE_RED={red}", *defines,
-               "-I", os.path.join(ROOT, "include"), "-I", _build.CSRC, "-cubin", "-o", cubin,
-               os.path.join(ROOT, "tools", "cta2_probe.cu")]
-        cmd = [c for c in cmd if c != "-Xcompiler,-fPIC,-O2,-Wall"]
-        subprocess.run(cmd, check=True, capture_output=True)
-        sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", cubin],
-                              capture_output=True, text=True).stdout
+    if not _probe_cache:
+        with tempfile.TemporaryDirectory() as d:
+            jobs = {}
+            for r in (0, 1, 2):
+                for k, defs in enumerate(_PROBE_DEFINES):
+                    cubin = os.path.join(d, f"probe_{r}_{k}.cubin")
+                    jobs[(r, defs)] = (cubin, subprocess.Popen(
+                        _probe_cmd(r, defs, cubin), stdout=subprocess.PIPE,
+                        stderr=subprocess.PIPE))
+            for key, (cubin, proc) in jobs.items():
+                out, err = proc.communicate()
+                assert proc.returncode == 0, err.decode()[-2000:]
+                _probe_cache[key] = subprocess.run(
+                    ["/usr/local/cuda/bin/cuobjdump", "-sass", cubin],
+                    capture_output=True, text=True).stdout
+    sass = _probe_cache[(red, tuple(defines))]
     funcs = [f for f in re.split(r"\n\s+Function : ", sass)[1:]
              if "sw2d_step_cta2" in f.split("\n", 1)[0]]
     assert len(funcs) == 1
