@@ -804,3 +804,25 @@ def test_persistent_kernels_of_two_handles_interleave_safely():
     finally:
         for h in hs:
             sw2d.sw2d_destroy(h)
+
+
+@pytest.mark.parametrize("rows", ["2", "5", "6", "7", "8", "11", "13"])
+@pytest.mark.parametrize("mask", [ALL, 0])
+def test_interior_row_loop_segment_lengths(rows, mask, monkeypatch):
+    """The two-step kernel runs a segment's first rows and last rows with the
+    row tests and the rows between without them (interior row
+    loop): segments of 2 .. 13 output rows put every transition (no interior,
+    one iteration of it, tails of 0-2 rows) at many places of the grid,
+    including the north / south walls — bitwise equal to the oracle, with and
+    without the per-step diagnostics."""
+    monkeypatch.setenv("SW2D_STEP_KERNEL", "1")
+    monkeypatch.setenv("SW2D_SK", "0")
+    monkeypatch.setenv("SW2D_MIN_ROWS", rows)
+    st = _bowl(250, 257)[1]
+    n = 20
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=mask)
+    assert_state_equal(got, want[:4], where=f"segments of {rows} rows")
+    if mask:
+        check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+        _check_history(hist, want[4], n)
