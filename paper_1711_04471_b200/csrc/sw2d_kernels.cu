@@ -348,6 +348,9 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 // predicate program the rule is (two compares with a predicate combine, one
 // 3-input predicate op, one select); ptxas otherwise if-converts it into a
 // chain of selects
+#ifndef SW2D_INTERIOR_SELECT
+#define SW2D_INTERIOR_SELECT 1  // interior commits without a lane branch (A/B: 0)
+#endif
 #ifndef SW2D_FACE_ARITH
 #define SW2D_FACE_ARITH 1   // 0: the predicate program below (A/B)
 #endif
@@ -672,6 +675,31 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
   vmul<C, kPack>(o.sS, w.w2, w.etC, x.nz);
 
   // a5: commit (lanes 1..30, rows of this segment)
+#if SW2D_INTERIOR_SELECT
+  if constexpr (!EDGE && C == 4 && RED <= 1) {
+    // interior rows: the stores predicated on the lane, the volume sum
+    // folded through a select (a halo lane adds +0): no divergent branch in
+    // the loop (C5 with VOLUME per step +5%; with all seven diagnostics the
+    // selects cost as much as the branch saves and spill the P2P variant, so
+    // RED = 2 keeps the branch)
+    if (x.out_lane) {
+      if constexpr (STORE) {
+        stC<C>(pU, un);
+        stC<C>(pV, vn);
+        stC<C>(pE, En);
+      }
+      if constexpr (REMOTE) {
+        remote_store(x, 1, L, un[0], un[1], un[2], un[3]);
+        remote_store(x, 2, L - 1, vn[0], vn[1], vn[2], vn[3]);
+        remote_store(x, 0, L - 2, En[0], En[1], En[2], En[3]);
+      }
+    }
+    if (RED >= 1) {
+      const float quad = __fadd_rn(__fadd_rn(En[0], En[1]), __fadd_rn(En[2], En[3]));
+      acc.sum_eta += (double)(x.out_lane ? quad : 0.0f);
+    }
+  } else
+#endif
   if (x.out_lane) {
     if (!EDGE || in_rows(L, x.ra, x.rb)) {
 #ifdef SW2D_DEBUG_BOUNDS
