@@ -45,9 +45,11 @@ struct Acc {
   double sum_eta;
   double wet;
   float max_eta, neg_min_eta, max_u, max_v;
+  int wet_i;   // wet cells counted in the row loop (exact; added to wet before the fold)
   __device__ void init() {
     sum_eta = 0.0;
     wet = 0.0;
+    wet_i = 0;
     max_eta = __int_as_float(0xff800000);  // -inf
     neg_min_eta = __int_as_float(0xff800000);
     max_u = 0.0f;
@@ -64,6 +66,7 @@ __device__ __forceinline__ double shfl_xor_d(double x, int m) {
 // order (deterministic) and writes the 7-double record.
 template <int LEVEL, int NW>
 __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
+  acc.wet += (double)acc.wet_i;
   __shared__ Acc sh[NW];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -159,6 +162,7 @@ __device__ void block_reduce_and_finalize(Acc acc, const RedArgs& r) {
 // path (no ticket, no last-CTA tail).
 template <int LEVEL, int NW>
 __device__ void block_reduce_to_partial(Acc acc, RedPartial* dst) {
+  acc.wet += (double)acc.wet_i;
   __shared__ Acc sh[NW];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __syncthreads();  // sh may still be read by a previous call
@@ -348,6 +352,9 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 // predicate program the rule is (two compares with a predicate combine, one
 // 3-input predicate op, one select); ptxas otherwise if-converts it into a
 // chain of selects
+#ifndef SW2D_INTERIOR_SELECT2
+#define SW2D_INTERIOR_SELECT2 1  // the select form for all seven diagnostics too (A/B: 0)
+#endif
 #ifndef SW2D_INTERIOR_SELECT
 #define SW2D_INTERIOR_SELECT 1  // interior commits without a lane branch (A/B: 0)
 #endif
@@ -676,7 +683,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
 
   // a5: commit (lanes 1..30, rows of this segment)
 #if SW2D_INTERIOR_SELECT
-  if constexpr (!EDGE && C == 4 && RED <= 1) {
+  if constexpr (!EDGE && C == 4 && (RED <= 1 || SW2D_INTERIOR_SELECT2)) {
     // interior rows: the stores predicated on the lane, the volume sum
     // folded through a select (a halo lane adds +0): no divergent branch in
     // the loop (C5 with VOLUME per step +5%; with all seven diagnostics the
@@ -697,6 +704,18 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
     if (RED >= 1) {
       const float quad = __fadd_rn(__fadd_rn(En[0], En[1]), __fadd_rn(En[2], En[3]));
       acc.sum_eta += (double)(x.out_lane ? quad : 0.0f);
+    }
+    if (RED >= 2) {   // (neutral values on halo lanes and outside columns)
+      const float ninf = __int_as_float(0xff800000);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const bool ok = x.out_lane && bit(x.colmask, c);
+        acc.max_u = fmaxf(acc.max_u, x.out_lane ? fabsf(un[c]) : 0.0f);
+        acc.max_v = fmaxf(acc.max_v, x.out_lane ? fabsf(vn[c]) : 0.0f);
+        acc.max_eta = fmaxf(acc.max_eta, ok ? En[c] : ninf);
+        acc.neg_min_eta = fmaxf(acc.neg_min_eta, ok ? -En[c] : ninf);
+        acc.wet_i += (ok && !(__fadd_rn(w.h0PP[c], En[c]) < x.hmin)) ? 1 : 0;
+      }
     }
   } else
 #endif
@@ -749,7 +768,7 @@ __device__ __forceinline__ void row_stepC(const WinT<C>& w, WinT<C>& o, const fl
           if (bit(x.colmask, c)) {
             acc.max_eta = fmaxf(acc.max_eta, En[c]);
             acc.neg_min_eta = fmaxf(acc.neg_min_eta, -En[c]);
-            acc.wet += (__fadd_rn(w.h0PP[c], En[c]) < x.hmin) ? 0.0 : 1.0;
+            acc.wet_i += (__fadd_rn(w.h0PP[c], En[c]) < x.hmin) ? 0 : 1;
           }
         }
       }
