@@ -124,6 +124,11 @@ void launch_step(const StepArgs& a, int red_level, int kind, void* stream,
 int step_occupancy_blocks_per_sm(int red_level, int kind);
 // Two steps per launch (kind 1 layout, one slab): state n -> n+2.
 void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote = false);
+// its three diagnostics levels, each built in a translation unit of its own
+// (sw2d_cta2_r0.cu, _r1.cu, _r2.cu)
+void launch_step2_r0(const StepArgs& a, void* stream, bool remote);
+void launch_step2_r1(const StepArgs& a, void* stream, bool remote);
+void launch_step2_r2(const StepArgs& a, void* stream, bool remote);
 int step2_strips_per_cta();
 void launch_step2_small(const StepArgs& a, int red_level, void* stream,
                         bool defer = false);  // kind 2, two steps

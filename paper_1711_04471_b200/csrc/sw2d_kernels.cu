@@ -1158,7 +1158,7 @@ constexpr int kCta2Strips = 7;
 constexpr int kCta2Threads = 32 * (kCta2Strips + 1);
 constexpr int kCta2WinBytes = (kCta2Strips * kColsPerStrip + 8) * 4;
 constexpr int kCta2StageBytes = 4 * kCta2WinBytes;
-constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
+[[maybe_unused]] constexpr int kCta2Smem = kCtaStages * kCta2StageBytes + 2 * 8 * kCtaStages;
 
 template <int RED, bool REMOTE>
 __global__ void __launch_bounds__(kCta2Threads, 1)
@@ -1770,6 +1770,27 @@ int grid_stride_blocks(long long n) {
 
 }  // namespace
 
+// (instantiated in sw2d_cta2_r0/1/2.cu, one diagnostics level per translation
+// unit: the three row-loop copies make each instance take minutes in ptxas)
+namespace {
+template <int RED, bool REMOTE>
+void launch_two(const StepArgs& a, cudaStream_t s) {
+  static unsigned long long attr_devices = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_devices >> (dev & 63) & 1ull)) {
+    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kCta2Smem);
+    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr_devices |= 1ull << (dev & 63);
+  }
+  const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
+  const int blocks = a.sk_ctas > 0 ? a.sk_ctas : ncc * a.nsegs;
+  sw2d_step_cta2<RED, REMOTE><<<blocks, kCta2Threads, kCta2Smem, s>>>(a);
+}
+}  // namespace
+
 #ifndef SW2D_PROBE   // tools/cta2_probe.cu: the kernels alone, one instantiation (SASS studies)
 int step_strips_per_cta(int kind) {
   return kind == 2 ? kSmallWarps : kCtaStrips;
@@ -1827,24 +1848,6 @@ int occupancy_kind(int kind) {
 }
 }  // namespace
 
-namespace {
-template <int RED, bool REMOTE>
-void launch_two(const StepArgs& a, cudaStream_t s) {
-  static unsigned long long attr_devices = 0;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!(attr_devices >> (dev & 63) & 1ull)) {
-    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kCta2Smem);
-    cudaFuncSetAttribute(sw2d_step_cta2<RED, REMOTE>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    attr_devices |= 1ull << (dev & 63);
-  }
-  const int ncc = (a.nstrips + kCta2Strips - 1) / kCta2Strips;
-  const int blocks = a.sk_ctas > 0 ? a.sk_ctas : ncc * a.nsegs;
-  sw2d_step_cta2<RED, REMOTE><<<blocks, kCta2Threads, kCta2Smem, s>>>(a);
-}
-}  // namespace
 
 int step2_strips_per_cta() { return kCta2Strips; }
 
@@ -1882,21 +1885,12 @@ int step2_small_occupancy_blocks_per_sm(int red_level) {
 }
 
 void launch_step2(const StepArgs& a, int red_level, void* stream, bool remote) {
-  cudaStream_t s = (cudaStream_t)stream;
-  if (remote) {
-    if (red_level >= 2)
-      launch_two<2, true>(a, s);
-    else if (red_level == 1)
-      launch_two<1, true>(a, s);
-    else
-      launch_two<0, true>(a, s);
-  } else if (red_level >= 2) {
-    launch_two<2, false>(a, s);
-  } else if (red_level == 1) {
-    launch_two<1, false>(a, s);
-  } else {
-    launch_two<0, false>(a, s);
-  }
+  if (red_level >= 2)
+    launch_step2_r2(a, stream, remote);
+  else if (red_level == 1)
+    launch_step2_r1(a, stream, remote);
+  else
+    launch_step2_r0(a, stream, remote);
 }
 
 void launch_step(const StepArgs& a, int red_level, int kind, void* stream, bool remote) {
