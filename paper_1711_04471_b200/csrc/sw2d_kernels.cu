@@ -347,11 +347,11 @@ __device__ __forceinline__ bool in_rows(int r, int lo, int hi) {
 // either way).
 // Wet/dry face rule (reading R4): the face between a cell with wet flag wc
 // and its east/north neighbour (wn) carries flow iff
-// wc ? (wn || d > 0) : (wn && d < 0); a blocked face gets 0.
-// face_flow(wc != 0, wn != 0, d) ? s : 0 for float wet flags, written as the
-// predicate program the rule is (two compares with a predicate combine, one
-// 3-input predicate op, one select); ptxas otherwise if-converts it into a
-// chain of selects
+// wc ? (wn || d > 0) : (wn && d < 0); a blocked face gets 0.  The row step
+// evaluates it as exact arithmetic, wc*wn + (wc - wn)*d > 0 (R26,
+// SW2D_FACE_ARITH); the A/B form below is the predicate program the rule is
+// (two compares with a predicate combine, one 3-input predicate op, one
+// select; ptxas otherwise if-converts the C++ into a chain of selects).
 #ifndef SW2D_INTERIOR_SELECT2
 #define SW2D_INTERIOR_SELECT2 1  // the select form for all seven diagnostics too (A/B: 0)
 #endif
