@@ -341,7 +341,7 @@ void plan_persist(sw2d* h) {
   struct Pick { int shape = -1, th = 0, ntx = 0, nty = 0; long long per_sm = 0; double cost = -1; };
   // the shape that minimises the busiest SM's work for K steps per block
   // (ties: the first, more warps)
-  auto pick = [&](int K) {
+  auto pick = [&](int K, bool lone_only) {
     Pick best;
     const int tw = persist_tile_cols(K);
     const int ntx = (int)((h->p.nx + tw - 1) / tw);
@@ -359,6 +359,7 @@ void plan_persist(sw2d* h) {
       // us/step, 8 x 24, 288 tiles 3.17 (3.58 vs 3.76 with VOLUME per step);
       // 16 x 32, 189 tiles 3.40; 16 x 48, 117 tiles 3.66.
       const long long per_sm = (nt + sms - 1) / sms;
+      if (lone_only && per_sm != 1) continue;
       const double cost = (double)persist_shape_rows(sh) * (double)per_sm *
                           (per_sm == 1 ? 1.5 : 1.0) *
                           (per_sm >= 4 && h->red_level == 0 ? 2.0 / 3.0 : 1.0);
@@ -373,15 +374,16 @@ void plan_persist(sw2d* h) {
     }
     return best;
   };
-  // K: 2, or 3 where the grid keeps several CTAs on every SM and no per-step
-  // partials are written (one handshake per three steps then pays for the
-  // wider apron: C2 3.03 -> 2.85 us/step with 16 warps x 32 rows; with a
-  // lone CTA per SM (C1) the phases' latency dominates and K = 3 is slower,
-  // 1.58 -> 2.07; with VOLUME per step within +-3%: profiles/ab_r02v.log)
+  // K: 2, or 3 where the K = 2 plan keeps several CTAs on every SM (one
+  // handshake per three steps then pays for the wider apron: C2 3.03 -> 2.85
+  // us/step with 16 warps x 32 rows; with a lone CTA per SM (C1) the phases'
+  // latency dominates and K = 3 is slower, 1.58 -> 2.07).  With per-step
+  // partials K = 3 wins only as one 16-warp CTA per SM (C2 VOLUME 3.54 ->
+  // 3.43, all 3.78 -> 3.74; as two 16-warp CTAs 3.64: profiles/ab_r02v.log)
   int K = K_force ? K_force : 2;
-  Pick p = pick(K);
-  if (!K_force && h->red_level == 0 && p.shape >= 0 && p.per_sm >= 2) {
-    const Pick p3 = pick(3);
+  Pick p = pick(K, false);
+  if (!K_force && p.shape >= 0 && p.per_sm >= 2) {
+    const Pick p3 = pick(3, h->red_level > 0);
     if (p3.shape >= 0) {
       K = 3;
       p = p3;
