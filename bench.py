@@ -396,8 +396,9 @@ def run_ours(args, cfg, ws, rank, local):
         hbm_achieved = alg_bytes / t_launch_s / 1e9
         peak, peak_src = hbm_peak()
         if persist:
-            kname = "sw2d_persist<%d, %s, %s, %d>" % (pk, plan["warps"], plan["rows_per_thread"],
-                                                      red_lvl)
+            kname = "sw2d_persist<%d, %s, %s, %d, %s>" % (
+                pk, plan["warps"], plan["rows_per_thread"], red_lvl,
+                "true" if plan.get("handshake") == "tagged" else "false")
         elif plan.get("kernel") == "small":
             kname = ("sw2d_step_small2<%d>" if spl == 2 else "sw2d_step_small<%d>") % red_lvl
         elif spl == 2:

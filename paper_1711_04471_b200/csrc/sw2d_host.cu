@@ -78,7 +78,9 @@ struct sw2d {
   // persistent cooperative kernel (small grids): K steps per shared-memory
   // block, pntx x pnty tiles of pth rows, one CTA each; pk = 0: off
   int pk = 0, pshape = 0, pth = 0, pntx = 0, pnty = 0;
+  bool ptag = false;   // tagged ring words instead of per-tile counters
   unsigned* pflags = nullptr;   // per-tile step counters
+  unsigned long long* pring = nullptr;   // tagged ring words (plans with one CTA per SM)
   unsigned pbase = 0;           // their value before the next launch
   RedPartial* ppart = nullptr;  // per-step CTA partials of one launch chunk
   std::vector<Slab> slabs;
@@ -322,6 +324,7 @@ float* fld(float* base, int64_t pitch, int64_t row) { return base + row * pitch;
 constexpr int kPersistRedChunk = 64;   // steps per launch when diagnostics are folded
 void plan_persist(sw2d* h) {
   h->pk = 0;
+  h->ptag = false;
   const long long cells = h->p.nx * h->p.ny;
   if (h->multi || h->virt || h->p.variant != SW2D_VARIANT_FUSED || h->slabs.size() != 1) return;
   if (cells > kSmallMaxCells) return;
@@ -390,6 +393,14 @@ void plan_persist(sw2d* h) {
     }
   }
   if (p.shape < 0) return;
+  // the handshake: tagged ring words on grids of few tiles (at most one per
+  // two SMs: the saved round trip is then the critical path and the polling
+  // light, C1 1.56 -> 1.46 us/step); per-tile counters otherwise (C2, 250
+  // tiles: 2.82 -> 3.20 tagged; with VOLUME per step, 140 tiles of 48 rows,
+  // 3.36 -> 3.52: every apron thread polling strains L2;
+  // profiles/ab_r02tagt_handshake.log).  SW2D_PERSIST_TAGGED=0/1 forces.
+  h->ptag = 2LL * p.ntx * p.nty <= sms;
+  if (const char* e = std::getenv("SW2D_PERSIST_TAGGED")) h->ptag = std::atoi(e) != 0;
   h->pk = K;
   h->pshape = p.shape;
   h->pth = p.th;
@@ -513,10 +524,11 @@ void plan_launches(sw2d* h) {
     if (h->pk) {
       std::snprintf(buf, sizeof(buf),
                     "kernel=persist steps_per_block=%d tiles=%dx%d tile=%dx%d warps=%d "
-                    "rows_per_thread=%d cooperative=1 halo=%s",
+                    "rows_per_thread=%d handshake=%s cooperative=1 halo=%s",
                     h->pk, h->pntx, h->pnty, persist_tile_cols(h->pk), h->pth,
                     persist_shape_warps(h->pshape),
                     persist_shape_rows(h->pshape) / persist_shape_warps(h->pshape),
+                    h->ptag ? "tagged" : "counters",
                     h->halo_mode == SW2D_HALO_P2P ? "p2p" : "nccl");
       h->plan_text = buf;
     }
@@ -865,6 +877,7 @@ void free_all(sw2d* h) {
   }
   cudaFree(h->sync);
   cudaFree(h->pflags);
+  cudaFree(h->pring);
   cudaFree(h->ppart);
   for (cudaEvent_t& e : h->ev_x)
     if (e) cudaEventDestroy(e);
@@ -1121,6 +1134,11 @@ int create_impl(sw2d* h, const sw2d_params* params, const sw2d_dist* dist,
     const size_t fw = persist_flag_words((int)nt);
     CUDA_TRY(h, cudaMalloc(&h->pflags, fw * sizeof(unsigned)));
     CUDA_TRY(h, cudaMemsetAsync(h->pflags, 0, fw * sizeof(unsigned), h->stream));
+    if (h->ptag) {   // tags start at 0: never a block's (its tag >= 1)
+      const size_t rw = persist_ring_words(h->p.nx, h->p.ny);
+      CUDA_TRY(h, cudaMalloc(&h->pring, rw * sizeof(unsigned long long)));
+      CUDA_TRY(h, cudaMemsetAsync(h->pring, 0, rw * sizeof(unsigned long long), h->stream));
+    }
     CUDA_TRY(h, cudaMalloc(&h->ppart, nt * (size_t)persist_shape_warps(h->pshape) *
                                           kPersistRedChunk * sizeof(RedPartial)));
   }
@@ -1630,6 +1648,8 @@ int sw2d_step(sw2d* h, int64_t nsteps) {
       a.nsteps = (int)chunk;
       a.flags = h->pflags;
       a.flag_base = h->pbase;
+      a.ring = h->pring;
+      a.ring_plane = h->p.nx * h->p.ny;
       a.c = h->coef;
       a.part = h->ppart;
       if (h->red_level) {

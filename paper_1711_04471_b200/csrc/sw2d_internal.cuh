@@ -219,7 +219,11 @@ struct PersistArgs {
   int cur;                   // buffer holding the state at the first step
   int nsteps;
   unsigned* flags;           // per tile: steps published (monotone across launches)
-  unsigned flag_base;        // the value every flag reached before this launch
+  unsigned flag_base;        // the value every flag reached before this launch (and
+                             // the tag base of the ring words)
+  unsigned long long* ring;  // tagged ring words [2][3][ny][nx] (tag << 32 | value
+                             // bits) instead of counters; nullptr: counters
+  long long ring_plane;      // nx * ny
   Coef c;
   RedPartial* part;          // [nsteps][ntiles] per-step CTA partials (RED >= 1)
 };
@@ -230,6 +234,7 @@ int persist_shape_warps(int shape);
 int persist_tile_cols(int K);
 int persist_tile_rows(int K, int shape);
 size_t persist_flag_words(int ntiles);   // flag array length (one 128-byte line per tile)
+size_t persist_ring_words(long long nx, long long ny);   // tagged ring words
 int persist_capacity(int K, int red_level, int shape);   // co-resident CTAs
 int launch_persist(const PersistArgs& a, int K, int red_level, void* stream);  // 0 or cudaError
 

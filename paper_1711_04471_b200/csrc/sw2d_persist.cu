@@ -59,6 +59,22 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Tagged ring words (PersistArgs::ring, plans with one CTA per SM): a value
+// and the step count it belongs to in one 8-byte word, stored and loaded as
+// single-copy-atomic relaxed accesses at gpu scope: a reader that sees the
+// tag it waits for sees that block's value — no counter, fence or CTA
+// barrier between a tile's ring stores and its neighbours' reloads.
+__device__ __forceinline__ void st_tagged(unsigned long long* p, unsigned tag, float v) {
+  const unsigned long long w =
+      ((unsigned long long)tag << 32) | (unsigned long long)__float_as_uint(v);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long* p) {
+  unsigned long long w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
 #ifndef SW2D_PERSIST_FACE_ARITH
 #define SW2D_PERSIST_FACE_ARITH 1
 #endif
@@ -104,7 +120,7 @@ struct PAcc {
 // ...); RW: shared rows per thread (the shared tile is PW RW rows)
 // (8 warps x 2 rows: at most 64 registers, so 4 CTAs fit an SM; 16 warps:
 // 64, so 2 fit)
-template <int K, int PW, int RW, int RED>
+template <int K, int PW, int RW, int RED, bool TAG>
 __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 ? 2 : 1))
     sw2d_persist(const PersistArgs a) {
   constexpr int A = 2 * K;            // apron cells per side
@@ -156,6 +172,11 @@ __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 
   auto gofs = [&](int y, int x) -> long long {
     return (long long)(gj0 + y - a.jbase) * pitch + (gk0 + x) + kColOff;
   };
+  // tagged ring words: [parity][field][ny][nx], field planes ring_plane apart
+  auto rofs = [&](int par, int y, int x) -> long long {
+    return (long long)par * 3 * a.ring_plane + (long long)(gj0 + y - 1) * nx + (gk0 + x - 1);
+  };
+  constexpr bool tagged = TAG;   // tagged ring words (a.ring) instead of counters
 
   int b = a.cur;   // buffer holding the current state
   // initial load: the whole apron'd tile (zero outside the grid)
@@ -345,6 +366,7 @@ __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 
     // Between blocks the neighbours read only the centre's outer ring (A
     // cells wide): that much is stored; after the last block all of it.
     const bool last = done >= a.nsteps;
+    const unsigned tag = a.flag_base + (unsigned)done;
 #pragma unroll
     for (int k = 0; k < RW; ++k) {
       const int y = wp + PW * k;
@@ -355,6 +377,13 @@ __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 
         const int x = c0 + c;
         if (x >= A && x < A + TW && colin[c] && (last || yring || x < 2 * A || x >= TW)) {
           const int i = y * kPX + x;
+          if (tagged && !last) {   // the ring as tagged words (parity b), not the state
+            unsigned long long* r = a.ring + rofs(b, y, x);
+            st_tagged(r, tag, sE[i]);
+            st_tagged(r + a.ring_plane, tag, sU[i]);
+            st_tagged(r + 2 * a.ring_plane, tag, sV[i]);
+            continue;
+          }
           const long long o = gofs(y, x);
           __stcg(a.E[b] + o, sE[i]);
           __stcg(a.U[b] + o, sU[i]);
@@ -363,6 +392,45 @@ __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 
       }
     }
     if (last) break;
+    if constexpr (tagged) {
+      // reload the apron straight from the neighbours' tagged words, each
+      // awaited by itself.  The words of parity b are rewritten two blocks
+      // later, after the neighbour consumed this tile's next ring, which was
+      // stored only after these loads returned (their values feed it)
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const int y = wp + PW * k;
+        const bool rowc = y >= A && y < A + TH;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int x = c0 + c;
+          if (rowc && x >= A && x < A + TW) continue;
+          const int i = y * kPX + x;
+          float e = 0.0f, u = 0.0f, v = 0.0f;
+          if (rowin[k] && colin[c]) {
+            const unsigned long long* r = a.ring + rofs(b, y, x);
+            unsigned long long we, wu, wv;
+            for (;;) {
+              we = ld_tagged(r);
+              wu = ld_tagged(r + a.ring_plane);
+              wv = ld_tagged(r + 2 * a.ring_plane);
+              if ((unsigned)(we >> 32) == tag && (unsigned)(wu >> 32) == tag &&
+                  (unsigned)(wv >> 32) == tag)
+                break;
+              __nanosleep(20);
+            }
+            e = __uint_as_float((unsigned)we);
+            u = __uint_as_float((unsigned)wu);
+            v = __uint_as_float((unsigned)wv);
+          }
+          sE[i] = e;
+          sU[i] = u;
+          sV[i] = v;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     __syncthreads();
     // (the barrier orders the CTA's stores before thread 0's release, which
     // is cumulative at gpu scope)
@@ -407,14 +475,14 @@ __global__ void __launch_bounds__(32 * PW, (PW == 8 && RW == 2) ? 4 : (PW == 16 
   }
 }
 
-template <int K, int PW, int RW, int RED>
+template <int K, int PW, int RW, int RED, bool TAG>
 void persist_attr() {
   static unsigned long long attr_devices = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_devices >> (dev & 63) & 1ull)) {
     // (static + dynamic shared memory must stay within 227 KB per CTA)
-    cudaFuncSetAttribute(sw2d_persist<K, PW, RW, RED>,
+    cudaFuncSetAttribute(sw2d_persist<K, PW, RW, RED, TAG>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, kPSmemMax);
     attr_devices |= 1ull << (dev & 63);
   }
@@ -423,24 +491,32 @@ void persist_attr() {
 constexpr size_t smem_of(int y) { return (size_t)8 * (size_t)y * kPX * sizeof(float); }
 
 template <int K, int PW, int RW, int RED>
-int capacity_t() {
-  persist_attr<K, PW, RW, RED>();
-  int per_sm = 0, sms = 0, dev = 0;
+int capacity_t() {   // co-resident CTAs of both handshake variants (the smaller)
+  persist_attr<K, PW, RW, RED, false>();
+  persist_attr<K, PW, RW, RED, true>();
+  int per_sm = 0, per_sm_t = 0, sms = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, PW, RW, RED>,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sw2d_persist<K, PW, RW, RED, false>,
+                                                    32 * PW, smem_of(PW * RW)) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, sw2d_persist<K, PW, RW, RED, true>,
                                                     32 * PW, smem_of(PW * RW)) != cudaSuccess) {
     cudaGetLastError();   // not sticky: the planner falls back
     return 0;
   }
-  return per_sm * sms;
+  return (per_sm < per_sm_t ? per_sm : per_sm_t) * sms;
 }
 
 template <int K, int PW, int RW, int RED>
 int launch_t(const PersistArgs& a, cudaStream_t s) {
-  persist_attr<K, PW, RW, RED>();
   void* args[] = {const_cast<PersistArgs*>(&a)};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)sw2d_persist<K, PW, RW, RED>,
+  const void* fn = a.ring ? (const void*)sw2d_persist<K, PW, RW, RED, true>
+                          : (const void*)sw2d_persist<K, PW, RW, RED, false>;
+  if (a.ring)
+    persist_attr<K, PW, RW, RED, true>();
+  else
+    persist_attr<K, PW, RW, RED, false>();
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn,
                                                     dim3((unsigned)(a.ntx * a.nty)),
                                                     dim3(32 * PW), args, smem_of(PW * RW), s);
   return e == cudaSuccess ? 0 : (int)e;
@@ -486,6 +562,7 @@ int persist_tile_rows(int K, int shape) {
 }
 int persist_tile_cols(int K) { return kPX - 4 * K; }
 size_t persist_flag_words(int ntiles) { return (size_t)ntiles * kPFlagStride; }
+size_t persist_ring_words(long long nx, long long ny) { return (size_t)6 * (size_t)nx * (size_t)ny; }
 
 // K = 3, 4 need more than 16 shared rows: shapes 0 and 3 have no usable tile
 // rows then (the planner skips them: persist_tile_rows <= 0)

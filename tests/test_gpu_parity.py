@@ -826,3 +826,35 @@ def test_interior_row_loop_segment_lengths(rows, mask, monkeypatch):
     if mask:
         check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
         _check_history(hist, want[4], n)
+
+
+@pytest.mark.parametrize("tag", ["0", "1"])
+@pytest.mark.parametrize("nx,ny,n,k,shape", [(100, 100, 61, "2", None), (500, 500, 40, "3", None),
+                                             (263, 97, 51, "2", "0"), (333, 140, 17, "3", "4"),
+                                             (130, 61, 33, "1", "2"), (3, 3, 7, "2", None)])
+def test_persistent_kernel_handshakes_bitwise(nx, ny, n, k, shape, tag, monkeypatch):
+    """Both handshakes between the persistent kernel's tiles — per-tile step
+    counters, and the ring as tagged 8-byte words polled directly (the
+    default where every SM holds one CTA) — forced on plans of one and of
+    several CTAs per SM: bitwise equal to the oracle with all diagnostics,
+    over chunked calls (the tags continue across launches)."""
+    monkeypatch.setenv("SW2D_PERSIST", "1")
+    monkeypatch.setenv("SW2D_PERSIST_K", k)
+    monkeypatch.setenv("SW2D_PERSIST_TAGGED", tag)
+    if shape:
+        monkeypatch.setenv("SW2D_PERSIST_SHAPE", shape)
+    h = sw2d.sw2d_create(sw2d.make_params(nx, ny, reduce_every_step=ALL, history_len=n))
+    try:
+        plan = sw2d.sw2d_plan(h)
+        assert "kernel=persist" in plan, plan
+        assert ("handshake=tagged" if tag == "1" else "handshake=counters") in plan, plan
+    finally:
+        sw2d.sw2d_destroy(h)
+    st = (si.generate(si.config("c1")) if (nx, ny) == (100, 100) else
+          si.generate(si.config("c2")) if (nx, ny) == (500, 500) else
+          _bowl(nx, ny)[1] if min(nx, ny) > 8 else _random_state(nx, ny))
+    want = oracle_run(P, st, n, history=True)
+    got, hist, red, _ = gpu_run(P, st, n, reduce_mask=ALL, chunks=[1, n // 2, n - 1 - n // 2])
+    assert_state_equal(got, want[:4], where=f"persistent K={k} handshake {tag} {nx}x{ny}")
+    check_reductions(red, oracle.reduce(P, st[0], *want[:3]))
+    _check_history(hist, want[4], n)
